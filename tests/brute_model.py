@@ -1,0 +1,113 @@
+"""An independently written, set-based model of the §8(c) semantics, used only to cross-check the oracle by
+brute-force enumeration.  It is deliberately structured differently from oracle/pool.py:
+sets and dicts instead of state arrays, provenance instead of bytes, counters recomputed from scratch.
+"""
+from __future__ import annotations
+
+INVAL, NOBLOCKS, NOHOST, HANDLE, BUSY = -1, -2, -3, -4, -5
+
+
+class Fail(Exception):
+    def __init__(self, status):
+        self.status = status
+
+
+class SetModel:
+    def __init__(self, N, S, ncls=2):
+        self.N, self.S = N, S
+        self.free = set(range(N))
+        self.pend = []                   # list of (cls, frozenset ids)
+        self.own = {}                    # id -> (agent, pos)
+        self.tab = {}                    # agent -> list
+        self.cls = {}
+        self.res = [0] * ncls
+        self.clm = [0] * ncls
+        self.stack = list(range(S))[::-1]
+        self.back = []
+        self.live = {}                   # handle -> (agent, cls, pos list, slot list)
+        self.dead = set()
+        self.nh = 0
+        self.prov = {b: b for b in range(N)}   # physical block -> original content id
+        self.hprov = {}
+
+    def _take(self, c, n):
+        unc = [max(0, self.res[x] - self.clm[x]) for x in range(len(self.res))]
+        from_res = unc[c] if unc[c] < n else n
+        if n > len(self.free) or n - from_res > max(0, len(self.free) - sum(unc)):
+            raise Fail(NOBLOCKS)
+        got = sorted(self.free)[:n]
+        self.clm[c] += from_res
+        self.free.difference_update(got)
+        return got
+
+    def add(self, a, c):
+        self.tab[a] = []
+        self.cls[a] = c
+
+    def reserve(self, c, n):
+        if sum(self.res) - self.res[c] + n > self.N:
+            raise Fail(INVAL)
+        self.res[c] = n
+
+    def alloc(self, a, n):
+        got = self._take(self.cls[a], n)
+        for b in got:
+            self.own[b] = (a, len(self.tab[a]))
+            self.tab[a].append(b)
+        return got
+
+    def offload(self, a, ids):
+        if not ids or len(set(ids)) < len(ids) or any(self.own.get(b, (None,))[0] != a for b in ids):
+            raise Fail(INVAL)
+        if len(self.stack) < len(ids):
+            raise Fail(NOHOST)
+        slots = []
+        pos = []
+        for b in ids:
+            s = self.stack.pop()
+            slots.append(s)
+            self.hprov[s] = self.prov[b]
+            p = self.own.pop(b)[1]
+            pos.append(p)
+            self.tab[a][p] = -1
+        self.pend.append((self.cls[a], frozenset(ids)))
+        self.nh += 1
+        self.live[self.nh] = (a, self.cls[a], pos, slots)
+        return self.nh
+
+    def upload(self, h):
+        if h not in self.live:
+            raise Fail(HANDLE)
+        a, c, pos, slots = self.live[h]
+        got = self._take(c, len(pos))
+        for p, s, b in zip(pos, slots, got):
+            self.prov[b] = self.hprov[s]
+            self.own[b] = (a, p)
+            self.tab[a][p] = b
+        self.back += slots
+        del self.live[h]
+        self.dead.add(h)
+        return got
+
+    def sync(self):
+        for c, ids in self.pend:
+            self.free |= ids
+            self.clm[c] = max(0, self.clm[c] - len(ids))
+        self.pend = []
+        self.stack += self.back
+        self.back = []
+
+    def agent_free(self, a):
+        if any(v[0] == a for v in self.live.values()):
+            raise Fail(BUSY)
+        mine = [b for b in self.tab[a] if b >= 0]
+        for b in mine:
+            del self.own[b]
+        self.free.update(mine)
+        c = self.cls[a]
+        self.clm[c] = max(0, self.clm[c] - len(mine))
+        self.tab[a] = []
+
+    def counts(self):
+        npend = sum(len(i) for _, i in self.pend)
+        return len(self.free), len(self.own), npend

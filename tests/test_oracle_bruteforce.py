@@ -1,0 +1,166 @@
+"""Brute force: every op sequence of depth <= 5 over a fixed 15-op alphabet on tiny pools,
+oracle vs the independent set-based model in tests/brute_model.py; plus all 2^8 subsets x 2 orders of C1's 8-block
+offload.  States already explored at the same remaining depth (identical oracle AND model state) are not
+re-expanded: their futures are identical by determinism, so every sequence's behaviour is still covered."""
+import copy
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle import BytesStore, OracleError, OraclePool
+from oracle.pool import OFFLOADED
+from workloads import content
+
+from brute_model import Fail, SetModel
+
+A, B = 0, 1
+ALPHABET = ([("alloc", a, n) for a in (A, B) for n in (1, 2)]
+            + [("offload", a, sel) for a in (A, B) for sel in ("all", "first")]
+            + [("upload", w) for w in ("oldest", "newest")]
+            + [("sync",)] + [("reserve", 0, n) for n in (0, 2)] + [("agent_free", a) for a in (A, B)])
+assert len(ALPHABET) == 15
+
+
+def sel_ids(table, sel):
+    on = [b for b in table if b >= 0]
+    return on if sel == "all" else on[:1]
+
+
+def run_oracle(p: OraclePool, op):
+    try:
+        k = op[0]
+        if k == "alloc":
+            return 0, p.alloc(op[1], op[2])
+        if k == "offload":
+            return 0, p.offload(op[1], sel_ids(p.block_table(op[1]), op[2]))
+        if k == "upload":
+            live = sorted(h for h, x in p.handles.items() if x.state == OFFLOADED)
+            h = (live[0] if op[1] == "oldest" else live[-1]) if live else 0
+            return 0, p.upload(h)
+        if k == "sync":
+            return 0, p.sync()
+        if k == "reserve":
+            return 0, p.reserve(op[1], op[2])
+        if k == "agent_free":
+            return 0, p.agent_free(op[1])
+    except OracleError as e:
+        return e.status, None
+    raise AssertionError(op)
+
+
+def run_model(m: SetModel, op):
+    try:
+        k = op[0]
+        if k == "alloc":
+            return 0, m.alloc(op[1], op[2])
+        if k == "offload":
+            return 0, m.offload(op[1], sel_ids(m.tab[op[1]], op[2]))
+        if k == "upload":
+            live = sorted(m.live)
+            h = (live[0] if op[1] == "oldest" else live[-1]) if live else 0
+            return 0, m.upload(h)
+        if k == "sync":
+            return 0, m.sync()
+        if k == "reserve":
+            return 0, m.reserve(op[1], op[2])
+        if k == "agent_free":
+            return 0, m.agent_free(op[1])
+    except Fail as e:
+        return e.status, None
+    raise AssertionError(op)
+
+
+def compare(p: OraclePool, m: SetModel, pool0, where):
+    s = p.stats()
+    assert (s["free"], s["alloc"], s["pending"]) == m.counts(), where
+    assert p.block_table(A) == m.tab[A] and p.block_table(B) == m.tab[B], where
+    assert p.reserved == m.res and p.claimed == m.clm, where
+    assert p.slot_free == m.stack and p.released_slots == m.back, where
+    live = {h: (x.agent, x.pos, x.slots) for h, x in p.handles.items() if x.state == OFFLOADED}
+    assert live == {h: (v[0], v[2], v[3]) for h, v in m.live.items()}, where
+    # payload: every physical block holds the original bytes of the model's provenance; live slots likewise
+    for b in range(m.N):
+        assert np.array_equal(p.store.pool[:, :, b], pool0[:, :, m.prov[b]]), (where, b)
+    for h, (_, _, _, slots) in m.live.items():
+        for sl in slots:
+            assert np.array_equal(p.store.host[sl], pool0[:, :, m.hprov[sl]]), (where, sl)
+
+
+def key(p: OraclePool, m: SetModel):
+    return (p.blk_state.tobytes(), p.owner.tobytes(), p.store.pool.tobytes(), p.store.host.tobytes(),
+            tuple(tuple(g.table) for g in p.agents.values()), tuple(p.reserved), tuple(p.claimed),
+            tuple(p.slot_free), tuple(p.released_slots), tuple(map(tuple, (x[1] for x in p.pending_dev))),
+            tuple((h, x.state, tuple(x.pos), tuple(x.slots)) for h, x in p.handles.items()), p.next_handle,
+            tuple(sorted(m.free)), tuple(sorted(m.prov.items())), tuple(sorted(m.hprov.items())),
+            tuple(m.stack), tuple(m.back), tuple(sorted(m.live)))
+
+
+def explore(N, S, depth):
+    pool0 = content.pool_bytes(9, 1, N, 1, 1, 8)          # C = 16 bytes per chunk
+    p = OraclePool(N, S, n_classes=2, store=BytesStore(pool0, S))
+    m = SetModel(N, S)
+    for a, c in ((A, 0), (B, 1)):
+        p.agent_add(a, c)
+        m.add(a, c)
+    seen = set()
+    nodes = [0]
+
+    def dfs(p, m, d, path):
+        if d == 0:
+            return
+        k = (d, key(p, m))
+        if k in seen:
+            return
+        seen.add(k)
+        for op in ALPHABET:
+            p2, m2 = copy.deepcopy(p), copy.deepcopy(m)
+            ro, rm = run_oracle(p2, op), run_model(m2, op)
+            nodes[0] += 1
+            where = path + [op]
+            assert ro == rm, (where, ro, rm)
+            compare(p2, m2, pool0, where)
+            dfs(p2, m2, d - 1, where)
+
+    dfs(p, m, depth, [])
+    return nodes[0], len(seen)
+
+
+@pytest.mark.parametrize("N,S,depth", [(4, 3, 5), (6, 4, 4)])
+def test_bruteforce_vs_set_model(N, S, depth):
+    n, states = explore(N, S, depth)
+    assert n > 1000 and states > 100
+
+
+@pytest.mark.slow
+def test_bruteforce_vs_set_model_deep():
+    explore(6, 4, 5)
+
+
+def test_c1_offload_all_subsets_both_orders():
+    """All 2^8 subsets x 2 orders of C1's 8-block offload, each followed by upload: round trip + ids."""
+    N, S = 64, 16
+    pool0 = content.pool_bytes(1, 1, N, 16, 2, 64)
+    for mask in range(1, 256):
+        for rev in (False, True):
+            p = OraclePool(N, S, store=BytesStore(pool0, S))
+            p.agent_add(0, 0); p.agent_add(1, 1)
+            for _ in range(8):
+                p.alloc(0, 1); p.alloc(1, 1)
+            tab = p.block_table(0)
+            pos = [i for i in range(8) if mask >> i & 1]
+            if rev:
+                pos = pos[::-1]
+            ids = [tab[i] for i in pos]
+            h = p.offload(0, ids)
+            p.sync()
+            new = p.upload(h)
+            # lowest free ids first, assigned in i order (A7): freed ids are exactly `ids`, plus 16.. upward
+            expect = sorted(set(range(16, N)) | set(ids))[:len(ids)]
+            assert new == expect
+            for i, b in zip(ids, new):
+                assert np.array_equal(p.store.pool[:, :, b], pool0[:, :, i])
+            t2 = p.block_table(0)
+            for q, b in zip(pos, new):
+                assert t2[q] == b
+            assert all(t2[i] == tab[i] for i in range(8) if i not in pos)

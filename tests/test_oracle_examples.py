@@ -1,0 +1,206 @@
+"""Oracle pins: SPEC worked examples, the hand-derived C1 worked example and quota pin (tests/golden/)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import (ALLOC, E_BUSY, E_HANDLE, E_INVAL, E_NOBLOCKS, E_NOHOST, FREE, PENDING, BytesStore, OracleError,
+                    OraclePool, ProvStore)
+from workloads import content
+from workloads.replay import Replayer
+from workloads.scripts import c1_worked_example
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def status_of(fn, *a):
+    try:
+        fn(*a)
+    except OracleError as e:
+        return e.status
+    return 0
+
+
+def full_state(p: OraclePool):
+    st = p.store
+    pay = (st.pool.copy(), st.host.copy()) if isinstance(st, BytesStore) else (st.prov.copy(), st.host_prov.copy())
+    return (pay, p.blk_state.copy(), p.owner.copy(), {a: (g.cls, list(g.table)) for a, g in p.agents.items()},
+            list(p.reserved), list(p.claimed), list(p.slot_free), list(p.released_slots),
+            [(c, list(i)) for c, i in p.pending_dev],
+            {h: (x.agent, x.state, list(x.pos), list(x.slots)) for h, x in p.handles.items()}, p.next_handle)
+
+
+def same(a, b):
+    if isinstance(a, np.ndarray):
+        return np.array_equal(a, b)
+    if isinstance(a, (tuple, list)):
+        return len(a) == len(b) and all(same(x, y) for x, y in zip(a, b))
+    return a == b
+
+
+# ------------------------------------------------------------------------------------------- SPEC examples
+def test_spec_allocate_examples():
+    g = gold("spec_block_memory_examples.json")
+    e = g["allocate_free10_req4"]
+    p = OraclePool(e["N"], 4); p.agent_add(0, 1)
+    p.alloc(0, e["request"])
+    assert p.stats()["free"] == e["expect_free"]
+
+    e = g["allocate_noncritical_headroom0"]
+    p = OraclePool(e["N"], 4); p.reserve(0, e["reserve_c0"]); p.agent_add(0, 1)
+    before = full_state(p)
+    assert status_of(p.alloc, 0, e["noncritical_request"]) == E_NOBLOCKS
+    assert same(before, full_state(p))                       # "pool unchanged"
+
+    e = g["allocate_critical_from_reservation"]
+    p = OraclePool(e["N"], 4); p.reserve(0, e["reserve_c0"]); p.agent_add(0, 0)
+    p.alloc(0, e["request"])
+    assert p.claimed[0] == e["expect_claimed"]
+
+
+def test_spec_free_reservation_first():
+    e = gold("spec_block_memory_examples.json")["free_reservation_first"]
+    # via agent_free: X holds 3, Y holds 2 (all claimed against class 0's reservation of 8)
+    p = OraclePool(16, 4); p.reserve(0, e["reserved"]); p.agent_add(0, 0); p.agent_add(1, 0)
+    p.alloc(0, 3); p.alloc(1, 2)
+    assert p.claimed[0] == e["claimed_before"]
+    p.agent_free(0)
+    assert p.claimed[0] == e["expect_claimed"]
+    # via offload retirement (S:141 + reading A10)
+    p = OraclePool(16, 8); p.reserve(0, e["reserved"]); p.agent_add(0, 0)
+    p.alloc(0, 5)
+    p.offload(0, p.block_table(0)[:3])
+    assert p.claimed[0] == 5                       # not yet: pending until sync
+    p.sync()
+    assert p.claimed[0] == e["expect_claimed"]
+
+
+def test_spec_zero_blocks_is_error():
+    p = OraclePool(8, 4); p.agent_add(0, 0); p.alloc(0, 2)
+    assert status_of(p.alloc, 0, 0) == E_INVAL
+    assert status_of(p.offload, 0, []) == E_INVAL
+
+
+def test_spec_offload_buffer_first_and_exhausted():
+    g = gold("spec_block_memory_examples.json")
+    e = g["offload_buffer_first"]
+    p = OraclePool(128, e["host_free_list"]); p.agent_add(0, 0); p.alloc(0, e["offload"])
+    p.offload(0, p.block_table(0))
+    s = p.stats()
+    assert s["host_free"] == e["expect_free_list"] and s["host_used"] == e["expect_in_use"]
+
+    p = OraclePool(16, 4, store=BytesStore(content.pool_bytes(1, 1, 16, 16, 2, 64), 4)); p.agent_add(0, 0)
+    p.alloc(0, 5)
+    before = full_state(p)
+    assert status_of(p.offload, 0, p.block_table(0)) == E_NOHOST
+    assert same(before, full_state(p))
+
+
+def test_spec_upload_stall_and_retry():
+    p = OraclePool(8, 8, store=BytesStore(content.pool_bytes(2, 1, 8, 16, 2, 64), 8))
+    p.agent_add(0, 0); p.agent_add(1, 1)
+    p.alloc(0, 4)
+    orig = p.store.pool[:, :, p.block_table(0)].copy()
+    h = p.offload(0, p.block_table(0)); p.sync()
+    p.alloc(1, 8)                                            # no free blocks left
+    before = full_state(p)
+    assert status_of(p.upload, h) == E_NOBLOCKS              # upload stalls
+    assert same(before, full_state(p))                       # handle stays valid, nothing changed
+    p.agent_free(1)
+    new = p.upload(h)
+    assert np.array_equal(p.store.pool[:, :, new], orig)
+    assert status_of(p.upload, h) == E_HANDLE                # single use
+
+
+# ------------------------------------------------------------------------------------------- C1 pins
+def test_c1_worked_example_golden():
+    g = gold("c1_worked_example.json")
+    N = g["N"]
+    pool0 = content.pool_bytes(1, 1, N, 16, 2, 64)
+    p = OraclePool(N, 16, store=BytesStore(pool0, 16))
+    A, F = g["agents"]["A"]["id"], g["agents"]["F"]["id"]
+    ops = c1_worked_example()
+    r = Replayer(p)
+    outs = []
+    for op in ops:
+        st, out = r.step(op)
+        assert st == 0, op
+        outs.append(out)
+        if op == ("offload", A, "all"):
+            assert p.block_table(A) == g["table_A_after_offload"]
+            assert p.block_table(F) == g["after_interleaved_alloc"]["F"]
+    assert outs[-5] == g["alloc_F_4_while_pending"]
+    assert outs[-3] == g["alloc_F_3_after_sync"]
+    assert outs[-2] == g["upload_new_ids"]
+    assert p.block_table(A) == g["upload_new_ids"]
+    s = p.stats()
+    assert {k: s[k] for k in ("free", "alloc", "pending")} == g["final_counts"]
+    for dst, src in g["final_bytes_provenance"].items():
+        assert np.array_equal(p.store.pool[:, :, int(dst)], pool0[:, :, src])
+
+
+def test_c1_interleaved_alloc_prefix():
+    g = gold("c1_worked_example.json")
+    p = OraclePool(64, 16); p.agent_add(0, 0); p.agent_add(1, 1)
+    for _ in range(8):
+        p.alloc(0, 1); p.alloc(1, 1)
+    assert p.block_table(0) == g["after_interleaved_alloc"]["A"]
+    assert p.block_table(1) == g["after_interleaved_alloc"]["F"]
+
+
+def test_c1_quota_pin():
+    g = gold("c1_quota_pin.json")
+    p = OraclePool(g["N"], 16)
+    ids = {"A": 0, "F": 1}
+    p.agent_add(0, 0); p.agent_add(1, 1)
+    for s in g["steps"]:
+        if s["op"] == "reserve":
+            p.reserve(s["cls"], s["n"])
+        elif "expect_status" in s:
+            assert status_of(p.alloc, ids[s["agent"]], s["n"]) == E_NOBLOCKS
+        else:
+            assert p.alloc(ids[s["agent"]], s["n"]) == s["expect_ids"]
+            if "expect_claimed0" in s:
+                assert p.claimed[0] == s["expect_claimed0"]
+
+
+def test_error_paths_leave_state_unchanged():
+    p = OraclePool(16, 4, store=BytesStore(content.pool_bytes(5, 1, 16, 16, 2, 64), 4))
+    p.agent_add(0, 0); p.agent_add(1, 0)
+    p.alloc(0, 3); p.alloc(1, 2)
+    t0 = p.block_table(0)
+    h = p.offload(0, t0[:2])
+    cases = [
+        (p.offload, 0, [t0[2], t0[2]]),           # duplicate ids
+        (p.offload, 0, [t0[0]]),                  # pending (already offloaded) block
+        (p.offload, 1, [t0[2]]),                  # block of another agent
+        (p.offload, 0, [99]),                     # out of range
+        (p.offload, 7, [t0[2]]),                  # unknown agent
+        (p.upload, h + 5),                        # unknown handle
+        (p.agent_free, 0),                        # BUSY: agent 0 has an offloaded handle
+        (p.reserve, 0, 17),                       # sum of reservations > N
+        (p.reserve, 9, 1),                        # unknown class
+        (p.agent_add, 1, 0),                      # duplicate agent
+        (p.alloc, 1, 0),
+    ]
+    expect = [E_INVAL, E_INVAL, E_INVAL, E_INVAL, E_INVAL, E_HANDLE, E_BUSY, E_INVAL, E_INVAL, E_INVAL, E_INVAL]
+    for (fn, *args), st in zip(cases, expect):
+        before = full_state(p)
+        assert status_of(fn, *args) == st, (fn.__name__, args)
+        assert same(before, full_state(p)), (fn.__name__, args)
+
+
+def test_block_states_and_location_flags():
+    p = OraclePool(8, 8); p.agent_add(0, 0); p.alloc(0, 3)
+    t = p.block_table(0)
+    p.offload(0, [t[1]])
+    assert p.blk_state[t[1]] == PENDING and p.block_table(0)[1] == -1
+    assert p.blk_state[t[0]] == ALLOC
+    p.sync()
+    assert p.blk_state[t[1]] == FREE
