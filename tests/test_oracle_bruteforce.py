@@ -126,7 +126,7 @@ def explore(N, S, depth):
     return nodes[0], len(seen)
 
 
-@pytest.mark.parametrize("N,S,depth", [(4, 3, 5), (6, 4, 4)])
+@pytest.mark.parametrize("N,S,depth", [(4, 3, 5), (6, 4, 5), (5, 2, 6)])
 def test_bruteforce_vs_set_model(N, S, depth):
     n, states = explore(N, S, depth)
     assert n > 1000 and states > 100
@@ -134,7 +134,7 @@ def test_bruteforce_vs_set_model(N, S, depth):
 
 @pytest.mark.slow
 def test_bruteforce_vs_set_model_deep():
-    explore(6, 4, 5)
+    explore(6, 4, 7)
 
 
 def test_c1_offload_all_subsets_both_orders():

@@ -66,12 +66,12 @@ C2 = Config("c2", "Qwen2.5-7B-shaped KV bf16, Code-Writer-style 16 agents stalli
 C3 = Config("c3", "Llama-3-8B-shaped KV bf16, Deep-Research-style 64 agents with Space-Scheduler partitions",
             L=32, H=8, D=128, dtype="bf16", N=32768, seed=3, n_agents=64,
             classes=("planner", "searcher", "summarizer", "writer"), quotas=((0, 0.10), (1, 0.05)),
-            bg_fill=0.70, med_blocks=256, sigma=0.6, clamp=(16, 512), per_cycle=8, stall_cycles=1,
+            bg_fill=0.20, med_blocks=256, sigma=0.6, clamp=(16, 512), per_cycle=8, stall_cycles=1,
             fill_chunk=8, host_frac=0.25)
 C4 = Config("c4", "Qwen2.5-32B-shaped KV bf16 head-sharded across 2/4/8 B200, 128 agents",
             L=64, H=8, D=128, dtype="bf16", N=32768, G=8, seed=4, n_agents=128,
             classes=("planner", "searcher", "summarizer", "writer"), quotas=((0, 0.10), (1, 0.05)),
-            bg_fill=0.70, med_blocks=128, sigma=0.8, clamp=(1, 2048), per_cycle=16, stall_cycles=1,
+            bg_fill=0.15, med_blocks=128, sigma=0.8, clamp=(1, 2048), per_cycle=16, stall_cycles=1,
             fill_chunk=8, host_frac=0.25)
 C5 = Config("c5", "Llama-3-70B-shaped KV bf16 on 8xB200, 256 agents at ~18% of the pool stalled, sweep 1-512",
             L=80, H=8, D=128, dtype="bf16", N=131072, G=8, seed=5, n_agents=256,
