@@ -1,0 +1,454 @@
+#!/usr/bin/env python
+"""Benchmark of the Tokencake offload/upload hot path on B200 (one process per GPU).
+
+A *step* is one scheduling cycle of the whole hot path: the cycle's uploads of agents
+whose function call is over (a5 allocation + a6 H2D scatter with the fused table remap), then the cycle's offloads of
+agents entering a function call (a2 admission + a3 gather/D2H), then the sync that retires pending blocks and returns
+host slots (a4, a7) — exactly the P:645-648 order, through the C ABI.
+
+  python bench.py [--gpus N --steps K --warmup W] [--workload c2|c3|c4|c5] [--mode auto|direct|staged]
+  python bench.py --impl reference ...     # the CPU oracle (oracle/), timed on the host cores
+
+Default workload: C2 (BASELINE.json configs[1], Qwen2.5-7B-shaped KV, Code-Writer-style 16 agents) on every rank —
+weak scaling over independent agent sets.  --workload c4/c5 runs the head-sharded 32B/70B configs (G = N ranks).
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads.configs import CONFIGS  # noqa: E402
+from workloads.scripts import CycleGen, setup_ops  # noqa: E402
+
+METRIC = "KV offload/upload GB/s and blocks/s per GPU vs host-link & HBM peak at 1/2/4/8 GPUs"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+HBM_FALLBACK = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback (GB/s), only if MEASURED_PEAKS.json is absent
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=None)
+    ap.add_argument("--mode", default="auto", choices=["auto", "direct", "staged"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--quick", action="store_true", help="skip host-link probe and device-tier microbench")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def workload_for(args, world):
+    name = args.workload or "c2"
+    cfg = CONFIGS[name]
+    sharded = name in ("c4", "c5")
+    G = world if sharded else 1
+    return cfg, G, ("strong" if sharded and world > 1 else "weak")
+
+
+# ------------------------------------------------------------------------------------------------- measurement aids
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.p = None
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:  # noqa: BLE001
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            out = self.p.communicate(timeout=5)[0]
+        except Exception:  # noqa: BLE001
+            self.p.kill()
+            out = ""
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0])); smax.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def hostlink_peak(torch, dev, nbytes=1 << 30, reps=5):
+    """Pinned cudaMemcpyAsync D2H / H2D / bidirectional, best of `reps`."""
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h2 = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def best(fn, nb):
+        fn(); torch.cuda.synchronize(dev)
+        b = 0.0
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(); fn(); e1.record(); e1.synchronize()
+            b = max(b, nb / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+        return b
+
+    def bidir():
+        cur = torch.cuda.current_stream(dev)
+        s1.wait_stream(cur); s2.wait_stream(cur)
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+        cur.wait_stream(s1); cur.wait_stream(s2)
+
+    r = {"h2d_gbs": best(lambda: d.copy_(h, non_blocking=True), nbytes),
+         "d2h_gbs": best(lambda: h.copy_(d, non_blocking=True), nbytes),
+         "bidir_gbs": best(bidir, 2 * nbytes), "bytes": nbytes, "how": "torch pinned copy_ 1 GiB, best of 5"}
+    del h, h2, d, d2
+    return r
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_PATH) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+    except Exception:  # noqa: BLE001
+        return HBM_FALLBACK, "B200_PROFILING.md fallback"
+
+
+# ------------------------------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import paper_2510_18586_b200 as tcb
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    cfg, G, scaling = workload_for(args, world)
+    shard_rank = rank if G > 1 else 0
+    mode = {"auto": tcb.XFER_AUTO, "direct": tcb.XFER_DIRECT, "staged": tcb.XFER_STAGED}[args.mode]
+    S = cfg.host_slots()
+
+    link = None if args.quick else hostlink_peak(torch, dev)
+    pool = tcb.Pool(cfg.L, cfg.H, cfg.D, cfg.T, cfg.dtype, cfg.N, device=local, shard_rank=shard_rank, shard_world=G,
+                    host_slots=S, max_agents=1024, max_blocks_per_agent=cfg.max_blocks_per_agent,
+                    xfer_d2h=mode, xfer_h2d=mode)
+    pool.fill(cfg.seed)
+    B = pool.block_bytes
+
+    # setup (untimed): quotas, agents, decode-like interleaved pre-fill — through the C ABI
+    ops, agents, _ = setup_ops(cfg)
+    for op in ops:
+        k = op[0]
+        if k == "reserve":
+            pool.reserve(op[1], op[2])
+        elif k == "agent_add":
+            pool.agent_add(op[1], op[2])
+        elif k == "alloc":
+            pool.alloc(op[1], op[2])
+        elif k == "agent_free":
+            pool.agent_free(op[1])
+        elif k == "sync":
+            pool.sync()
+    gen = CycleGen(cfg, agents)
+    handles = {}
+
+    def cycle(record=None):
+        """One scheduling cycle through the public API; returns (blocks_up, blocks_off)."""
+        cyc = gen.next_cycle()
+        nu = no = 0
+        for op in cyc:
+            if op[0] == "upload_batch":
+                hs = np.array([handles.pop(a) for a in op[1]], dtype=np.uint64)
+                sizes = [pool.handle_info(int(h))[1] for h in hs]
+                offs = np.zeros(len(hs) + 1, dtype=np.int64); offs[1:] = np.cumsum(sizes)
+                out = np.empty(int(offs[-1]), dtype=np.int32)
+                pool.upload_batch_arrays(hs, offs, out)
+                nu += int(offs[-1])
+            elif op[0] == "offload_batch":
+                ags = np.array([a for a, _ in op[1]], dtype=np.int32)
+                tabs = [np.asarray(pool.block_table(int(a)), dtype=np.int32) for a in ags]
+                tabs = [t[t >= 0] for t in tabs]
+                offs = np.zeros(len(tabs) + 1, dtype=np.int64); offs[1:] = np.cumsum([len(t) for t in tabs])
+                ids = np.ascontiguousarray(np.concatenate(tabs))
+                if record is not None:
+                    record("pre_offload")
+                hs = pool.offload_batch_arrays(ags, offs, ids)
+                for a, h in zip(ags, hs):
+                    handles[int(a)] = int(h)
+                no += int(offs[-1])
+            elif op[0] == "sync":
+                if record is not None:
+                    record("end")
+                pool.sync()
+        return nu, no
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    up_s, off_s = pool.streams()
+    ups, offs_ = torch.cuda.ExternalStream(up_s, device=dev), torch.cuda.ExternalStream(off_s, device=dev)
+
+    for _ in range(cfg.stall_cycles + 1):      # prime: get stalled agents to upload
+        cycle()
+    for _ in range(args.warmup):
+        cycle()
+    pool.timing(True)
+    pool.timing(True)                          # reset accumulators
+    launches0 = pool.stats()["kernel_launches"]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = Clocks(local)
+    dev_ms, host_ms, bytes_up, bytes_off, blocks = [], [], 0, 0, 0
+    t_wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        flush.zero_()                          # flush L2 between steps (outside the step's events)
+        torch.cuda.synchronize(dev)
+        ev = {}
+
+        def record(tag):
+            if tag == "end":
+                for nm, st in (("up1", ups), ("off1", offs_)):
+                    e = torch.cuda.Event(enable_timing=True); e.record(st); ev[nm] = e
+        for nm, st in (("up0", ups), ("off0", offs_)):
+            e = torch.cuda.Event(enable_timing=True); e.record(st); ev[nm] = e
+        t0 = time.perf_counter()
+        nu, no = cycle(record)
+        t1 = time.perf_counter()
+        ref = ev["up0"]
+        start = min(0.0, ref.elapsed_time(ev["off0"]))
+        end = max(ref.elapsed_time(ev["up1"]), ref.elapsed_time(ev["off1"]))
+        dev_ms.append(end - start)
+        host_ms.append((t1 - t0) * 1e3)
+        bytes_up += nu * B
+        bytes_off += no * B
+        blocks += nu + no
+    torch.cuda.synchronize(dev)
+    t_wall = time.perf_counter() - t_wall0
+    clk = clocks.stop()
+    tim = pool.timing(False)
+    launches = pool.stats()["kernel_launches"] - launches0
+
+    my = torch.tensor([sum(dev_ms), sum(host_ms), bytes_up + bytes_off, blocks, t_wall], dtype=torch.float64,
+                      device=dev)
+    tot = my.clone()
+    if dist is not None:
+        mx = my.clone(); dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = my.clone(); dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        tot = torch.stack([mx[0], mx[1], sm[2], sm[3], mx[4]])
+    dev_total_ms, host_total_ms, all_bytes, all_blocks, wall = [float(x) for x in tot.cpu()]
+
+    hbm, hbm_src = hbm_peak()
+    dev_bench = None if args.quick else device_tier_bench(torch, pool, cfg, dev, hbm, hbm_src)
+    if rank != 0:
+        if dist is not None:
+            dist.barrier(); dist.destroy_process_group()
+        return
+
+    value = all_bytes / (dev_total_ms * 1e-3) / 1e9
+    e2e = all_bytes / (host_total_ms * 1e-3) / 1e9
+    # roofline of the dominant kernel: per-launch algorithmic bytes / event-timed launch duration
+    kern = {}
+    for k, peak_key in (("offload_kernel", "d2h_gbs"), ("upload_kernel", "h2d_gbs")):
+        ms, cnt, byt = tim[k]
+        if cnt:
+            kern[k] = {"ms_total": ms, "launches": cnt, "bytes_per_launch": byt / cnt,
+                       "achieved_gbs": byt / (ms * 1e-3) / 1e9, "peak_key": peak_key}
+    for k in ("memcpy_d2h", "memcpy_h2d"):
+        ms, cnt, byt = tim[k]
+        if cnt:
+            kern[k] = {"ms_total": ms, "runs": cnt, "achieved_gbs": byt / (ms * 1e-3) / 1e9}
+    stats = pool.stats()
+    staged = stats["xfer_d2h"] == tcb.XFER_STAGED
+    roof = None
+    if kern:
+        dom = max((k for k in kern if k.endswith("_kernel")), key=lambda k: kern[k]["ms_total"])
+        kd = kern[dom]
+        if staged:   # device-side gather/scatter: HBM-bound, read + write bytes
+            ach = 2 * kd["achieved_gbs"]
+            roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                    "traffic": None, "peak_source": hbm_src}
+        else:        # direct mapped-host kernel: bound by the host link (PCIe Gen5 x16)
+            pk = link[kd["peak_key"]] if link else None
+            roof = {"kernel": dom, "bound": "host_link", "achieved": kd["achieved_gbs"], "peak": pk, "unit": "GB/s",
+                    "frac": (kd["achieved_gbs"] / pk) if pk else None, "traffic": None,
+                    "peak_source": "live pinned cudaMemcpyAsync 1 GiB in this run (" +
+                                   ("D2H" if dom == "offload_kernel" else "H2D") + ")"}
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cpu = cpu_baseline(cfg, args.cpu_seconds)
+    n_steps = args.steps
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": n_steps, "warmup": args.warmup,
+        "ms_per_step": dev_total_ms / n_steps, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+        "dtype": "u16 (bit copy of bf16 KV)", "data": "synthetic (splitmix64 KV contents, seeded op scripts)",
+        "config": {"workload": f"{cfg.name}: {cfg.title}", "layers": cfg.L, "kv_heads": cfg.H, "head_dim": cfg.D,
+                   "block_tokens": cfg.T, "head_shards": G, "n_blocks": cfg.N, "block_shard_bytes": B,
+                   "host_slots": S, "agents": cfg.n_agents, "per_cycle": cfg.per_cycle,
+                   "xfer": {1: "direct", 2: "staged"}[stats["xfer_d2h"]] + "/" +
+                           {1: "direct", 2: "staged"}[stats["xfer_h2d"]],
+                   "l2": "flushed between steps (256 MiB write, outside the step events)",
+                   "parallelism": f"{world} independent ranks" + (f", head-sharded G={G}" if G > 1 else "")},
+        "blocks_per_s": all_blocks / (dev_total_ms * 1e-3),
+        "bytes_per_step": all_bytes / n_steps,
+        "gpu_launches": int(launches),
+        "kernels": kern,
+        "hostlink_peak": link,
+        "roofline": roof,
+        "roofline_device": dev_bench,
+        "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": (bytes_up + 16 * all_blocks) / n_steps,
+                "d2h_bytes_per_step": bytes_off / n_steps,
+                "how": "host wall clock around the public-API cycle (upload_batch, offload_batch, sync) per step"},
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier(); dist.destroy_process_group()
+
+
+def device_tier_bench(torch, pool, cfg, dev, hbm, hbm_src):
+    """Device-side gather (KG1) and scatter (KS1) alone, >= 256 MiB per launch, event-timed (HBM roofline)."""
+    B = pool.block_bytes
+    n = max(1, (512 << 20) // B)
+    rng = np.random.default_rng(7)
+    ids = rng.choice(cfg.N, size=n, replace=False).astype(np.int32)
+    dst = torch.empty(n * B, dtype=torch.uint8, device=dev)
+    s = torch.cuda.Stream(dev)
+    out = {}
+    for name, fn in (("gather", lambda: pool.gather_dev(ids, dst.data_ptr(), s.cuda_stream)),
+                     ("scatter", lambda: pool.scatter_dev(dst.data_ptr(), ids, s.cuda_stream))):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize(dev)
+        ts = []
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s); fn(); e1.record(s); e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = statistics.median(ts)
+        ach = 2 * n * B / (ms * 1e-3) / 1e9
+        out[name] = {"bytes_per_launch": n * B, "ms": ms, "achieved": ach, "frac": ach / hbm}
+    return {"bound": "hbm", "unit": "GB/s (read+write)", "peak": hbm, "peak_source": hbm_src, **out}
+
+
+# ------------------------------------------------------------------------------------------------- CPU oracle
+def oracle_setup(cfg):
+    """Scaled copy of the workload for the host: same per-agent sizes and per-cycle counts, smaller N."""
+    from oracle import BytesStore, OraclePool
+    N = 1536 if cfg.block_bytes(1) <= (1 << 20) else 768
+    small = cfg.scaled(N=N, host_slots=int(N * 0.45), bg_fill=0.25)
+    C = small.chunk_bytes(1)
+    pool0 = np.empty((small.L, 2, N, C), dtype=np.uint8)
+    pool0.reshape(-1)[:] = np.arange(pool0.size, dtype=np.uint64).astype(np.uint8)   # content irrelevant to timing
+    o = OraclePool(N, small.host_slots(), max_agents=1024, max_blocks_per_agent=small.max_blocks_per_agent,
+                   store=BytesStore(pool0, small.host_slots()))
+    from workloads.replay import Replayer
+    ops, agents, _ = setup_ops(small)
+    Replayer(o).run(ops)
+    return small, o, agents
+
+
+def oracle_cycles(small, o, agents, seconds=None, steps=None, warmup=0):
+    from workloads.replay import Replayer
+    gen = CycleGen(small, agents)
+    r = Replayer(o)
+    for a in agents:
+        r.handles.setdefault(a, __import__("collections").deque())
+    B = small.block_bytes(1)
+
+    def one():
+        nb = 0
+        for op in gen.next_cycle():
+            st, out = r.step(op)
+            assert st == 0, op
+            if op[0] == "upload_batch":
+                nb += sum(len(x) for x in out)
+            elif op[0] == "offload_batch":
+                nb += sum(r.pool.handles[h].pos.__len__() for h in out)
+        return nb
+
+    for _ in range(small.stall_cycles + 1 + warmup):
+        one()
+    t0 = time.perf_counter()
+    times, blocks = [], 0
+    while True:
+        s = time.perf_counter()
+        blocks += one()
+        times.append(time.perf_counter() - s)
+        if steps is not None and len(times) >= steps:
+            break
+        if seconds is not None and time.perf_counter() - t0 >= seconds:
+            break
+    return blocks * B, sum(times), len(times)
+
+
+def cpu_baseline(cfg, seconds):
+    small, o, agents = oracle_setup(cfg)
+    nbytes, secs, cycles = oracle_cycles(small, o, agents, seconds=seconds)
+    return {"value": nbytes / secs / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"{cycles} cycles of {cfg.name} per-agent sizes on a host-scaled pool (N={small.N}, "
+                      f"{small.host_slots()} slots), NumPy BytesStore, single thread, {secs:.1f} s",
+            "host_cpu_count": os.cpu_count()}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cfg, G, scaling = workload_for(args, 1)
+    small, o, agents = oracle_setup(cfg)
+    nbytes, secs, cycles = oracle_cycles(small, o, agents, steps=args.steps, warmup=args.warmup)
+    value = nbytes / secs / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3 / cycles, "higher_is_better": True,
+        "scaling": scaling, "vs_baseline": None, "dtype": "u16 (bit copy of bf16 KV)", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.title}", "host_scaled_n_blocks": small.N,
+                   "block_shard_bytes": small.block_bytes(1)},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{cycles} cycles on a host-scaled pool (N={small.N})"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -1,0 +1,185 @@
+/*
+ * tokencake.h — C ABI of the B200-native Tokencake Time-Scheduler hot path (arXiv 2510.18586).
+ *
+ * What it does (§4 "The Time Scheduler", and §Implementation): while an agent stalls on
+ * a function call, its paged KV-cache blocks — non-contiguous (block, layer, K|V) chunks of a layer-major pool — are
+ * gathered into pinned host memory taken from an internal free list ("CPU Block Buffering"); the source
+ * GPU blocks become "pending free" and return to the pool only after the transfer completes.  Before the call
+ * returns they are scattered back into freshly allocated GPU blocks and the agent's block table is remapped
+ * (P:388).  Allocation honours the Space Scheduler's per-class reservations: a shared pool plus a
+ * reserved pool per critical agent class (Alg. 2 line 15 reserve_num[agent_type]).
+ *
+ * Conventions:
+ *  - One pool per (process, CUDA device).  Not thread-safe: a single writer, as S:204-205.
+ *  - Ownership: the caller owns every array it passes; inputs are copied before return; outputs are written only on
+ *    TC_OK.  Handles, pinned host slots, streams, events and (unless supplied externally) device memory are owned by
+ *    the library and released by tc_pool_destroy.
+ *  - Errors: strong guarantee — a non-OK status other than TC_E_CUDA leaves every piece of state unchanged.
+ *    TC_E_NOHOST (offload refused) and TC_E_NOBLOCKS (upload "stalls"; the handle stays valid) are
+ *    recoverable: retry after sync / free / re-quota.  TC_E_CUDA is sticky: the pool refuses further work and
+ *    tc_last_error() says why.
+ *  - Asynchrony: tc_offload / tc_upload return once the work is enqueued on the library's copy streams.  Logical
+ *    state (block tables, counters) changes at call time; device/host bytes are valid after tc_wait / tc_stream_wait
+ *    / tc_sync.  Freed device blocks and released host slots are reusable only after tc_sync (reading A8), so every
+ *    id is a pure function of the call sequence, never of copy timing.
+ *  - Layouts: KV pool [L][2][N][T][H/G][D] of 16-bit words (layer-major; chunk (block, layer, K|V) = C contiguous
+ *    bytes, C = T*(H/G)*D*2; reading A3).  A host slot holds one block shard [L][2][C] = B = 2*L*C bytes (A4).
+ *    Device block table int32[max_agents][max_blocks_per_agent], -1 = on host (A17).
+ *  - Payload is opaque 16-bit words: never converted; NaN payloads, -0 and denormals survive (A14).
+ */
+#ifndef TOKENCAKE_H
+#define TOKENCAKE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tc_pool tc_pool;      /* opaque, library-owned */
+typedef uint64_t tc_handle;          /* 0 = none; issued 1, 2, 3, ... in call order */
+
+typedef enum { TC_FP16 = 0, TC_BF16 = 1 } tc_dtype;
+
+typedef enum {
+    TC_OK = 0,
+    TC_E_INVAL = -1,     /* bad argument: n < 1, duplicate ids, id not an on-GPU block of the agent, unknown agent /
+                            class, sum of reservations > N, table row capacity exceeded (A15, A5, A9, A22) */
+    TC_E_NOBLOCKS = -2,  /* not enough free device blocks under the partition rule; nothing changed */
+    TC_E_NOHOST = -3,    /* host block buffer exhausted; offload refused, nothing changed */
+    TC_E_HANDLE = -4,    /* unknown handle, or already uploaded */
+    TC_E_BUSY = -5,      /* agent_free while the agent has offloaded blocks / query: transfer still running */
+    TC_E_CUDA = -6,      /* CUDA error (sticky); see tc_last_error */
+    TC_E_OOM = -7,       /* device or pinned-host allocation failed at create time */
+    TC_E_NODEV = -8      /* operation needs KV storage but the pool is metadata-only (device = -1) */
+} tc_status;
+
+typedef enum {
+    TC_XFER_AUTO = 0,    /* per direction: the path the library measured faster at create time (tc_calibrate) */
+    TC_XFER_DIRECT = 1,  /* one SM kernel reads/writes mapped pinned host memory over the host link */
+    TC_XFER_STAGED = 2   /* SM gather/scatter to a device staging ring + copy-engine cudaMemcpyAsync */
+} tc_xfer_mode;
+
+typedef struct tc_pool_desc {
+    int32_t layers, kv_heads, head_dim, block_tokens;
+    tc_dtype dtype;
+    int64_t n_blocks;            /* N: blocks in this GPU's pool */
+    int32_t device;              /* CUDA ordinal; -1 = metadata-only pool: allocator, tables and handles without KV
+                                    storage or transfers (host-logic testing; data ops return TC_E_NODEV) */
+    int32_t shard_rank, shard_world;   /* head shard: local heads = kv_heads / shard_world (must divide), A19 */
+    int64_t host_slots;          /* S: pinned host block-shard slots; 0 -> ceil(0.18 * N) */
+    int32_t n_classes;           /* agent classes, 1..64; 0 -> 8 */
+    int32_t max_agents;          /* block-table rows; 0 -> 1024 */
+    int32_t max_blocks_per_agent;/* block-table row capacity; 0 -> 4096 */
+    void *kv_dev;                /* optional external device buffer (e.g. torch-allocated) >= L*2*N*C bytes,
+                                    16-byte aligned; NULL -> library cudaMalloc */
+    int32_t *table_dev;          /* optional external device int32[max_agents][max_blocks_per_agent]; NULL -> own */
+    int32_t xfer_d2h, xfer_h2d;  /* tc_xfer_mode per direction */
+    int64_t staging_bytes;       /* device staging ring per direction for STAGED mode; 0 -> 256 MiB */
+    int64_t desc_bytes;          /* pinned descriptor ring; 0 -> 16 MiB */
+} tc_pool_desc;
+
+typedef struct tc_stats_t {
+    int64_t n_blocks, free_blocks, alloc_blocks, pending_blocks;
+    int64_t host_slots, host_free, host_used, host_released;
+    int64_t chunk_bytes, block_bytes;
+    int32_t n_classes, n_agents;
+    int64_t reserved[64], claimed[64];
+    int64_t live_handles;
+    int64_t kernel_launches, memcpy_calls;     /* cumulative, this pool */
+    int64_t bytes_d2h, bytes_h2d;              /* cumulative KV payload bytes enqueued */
+    int32_t xfer_d2h, xfer_h2d;                /* effective modes (AUTO resolved) */
+} tc_stats_t;
+
+/* ---- pool lifecycle ------------------------------------------------------------------------------------------ */
+/* Fill *d with defaults for the given geometry (device = current CUDA device). */
+void tc_pool_desc_init(tc_pool_desc *d, int32_t layers, int32_t kv_heads, int32_t head_dim, int32_t block_tokens,
+                       tc_dtype dtype, int64_t n_blocks);
+/* P:601 paged pool (vLLM PagedAttention): N blocks of T tokens x all layers x K,V x local heads x head_dim. */
+tc_status tc_pool_create(int32_t layers, int32_t kv_heads, int32_t head_dim, int32_t block_tokens, tc_dtype dtype,
+                         int64_t n_blocks, tc_pool **out);
+tc_status tc_pool_create_ex(const tc_pool_desc *d, tc_pool **out);
+void tc_pool_destroy(tc_pool *p);
+/* Device KV base pointer (layout above) and chunk bytes C. */
+tc_status tc_pool_kv(tc_pool *p, void **kv_dev, int64_t *chunk_bytes);
+/* Offloads wait (GPU-side) for work already queued on this stream, so an agent's last decode writes are captured. */
+tc_status tc_set_compute_stream(tc_pool *p, void *cuda_stream);
+/* The library's copy streams (upload = high priority), for event timing / dependencies by the caller. */
+tc_status tc_streams(tc_pool *p, void **upload_stream, void **offload_stream);
+/* Override the transfer mode per direction (tc_xfer_mode) for subsequent calls. */
+tc_status tc_set_xfer_mode(tc_pool *p, int32_t d2h, int32_t h2d);
+/* Synthetic content: every 8-byte word of the unsharded pool = splitmix64(widx + seed*0xD1B54A32D192ED03), widx its
+   index in [L][2][N][T][H][D]; this rank writes its head shard.  Tests/bench only. */
+tc_status tc_fill_kv(tc_pool *p, uint64_t seed);
+
+/* ---- Space-Scheduler partition + agents (a1, a5) ------------------------------------------------------------ */
+/* reserve_num[agent_class] = n_blocks.  Counts, not address ranges (A9).  Requires sum over classes <= N.
+   claimed is untouched: a shrink below claimed is lazy. */
+tc_status tc_partition_reserve(tc_pool *p, int32_t agent_class, int64_t n_blocks);
+tc_status tc_agent_add(tc_pool *p, int32_t agent, int32_t agent_class);
+/* Decode growth: append n blocks to the agent's table; ids = lowest free first (A7), reservation first then shared
+   headroom = free - sum of unclaimed reservations.  out_ids[n] receives them. */
+tc_status tc_alloc(tc_pool *p, int32_t agent, int64_t n, int32_t *out_ids);
+/* Release all the agent's on-GPU blocks (reservation-first return).  TC_E_BUSY while it has offloaded
+   blocks.  The caller guarantees no queued compute still uses them. */
+tc_status tc_agent_free(tc_pool *p, int32_t agent);
+
+/* ---- the hot path (a2-a8) ----------------------------------------------------------------------------------- */
+/* a2+a3: offload block_ids[0..n) (on-GPU blocks exclusively owned by the agent) to pinned host slots from the
+   CPU block buffer; gather all 2L chunks of each block in one kernel launch; table entries -> -1 (device table
+   written by the kernel epilogue); source blocks PENDING until tc_sync.  *out = new handle. */
+tc_status tc_offload(tc_pool *p, int32_t agent, const int32_t *block_ids, int64_t n, tc_handle *out);
+/* a5+a6: allocate n new blocks (rule of tc_alloc) and scatter the handle's host copy into them; the kernel's fused
+   epilogue writes table[agent][pos_i] = out_new_ids[i] (new_ids[i] replaces block_ids[i], A6).  Upload waits
+   (GPU-side) for the handle's offload (A13).  NOBLOCKS: nothing changes, the handle stays valid. */
+tc_status tc_upload(tc_pool *p, tc_handle h, int32_t *out_new_ids);
+/* a8: one scheduling cycle's offloads as ONE launch.  Agent k offloads block_ids[offsets[k]..offsets[k+1]).
+   All-or-nothing. out_handles[n_agents]. */
+tc_status tc_offload_batch(tc_pool *p, int32_t n_agents, const int32_t *agents, const int64_t *offsets,
+                           const int32_t *block_ids, tc_handle *out_handles);
+/* a8: one cycle's uploads as ONE launch; offsets[n_handles+1] must match each handle's block count (see
+   tc_handle_info).  Sequential-composition semantics, all-or-nothing.  out_new_ids[offsets[n_handles]]. */
+tc_status tc_upload_batch(tc_pool *p, int32_t n_handles, const tc_handle *hs, const int64_t *offsets,
+                          int32_t *out_new_ids);
+/* TC_OK if the handle's last transfer has completed, TC_E_BUSY if not, TC_E_HANDLE if unknown. */
+tc_status tc_query(tc_pool *p, tc_handle h);
+tc_status tc_wait(tc_pool *p, tc_handle h);                        /* host-blocking */
+tc_status tc_stream_wait(tc_pool *p, tc_handle h, void *cuda_stream); /* GPU-side dependency, no host block */
+/* Drain both copy streams; retire PENDING device blocks (FREE, claimed -= min(n, claimed)) in issue order, then
+   return released host slots to the free list.  Uploaded handles are forgotten. */
+tc_status tc_sync(tc_pool *p);
+
+/* ---- queries ------------------------------------------------------------------------------------------------- */
+tc_status tc_block_table(tc_pool *p, int32_t agent, int32_t *out, int64_t cap, int64_t *n_out); /* -1 = on host */
+tc_status tc_block_table_dev(tc_pool *p, int32_t **dev_table, int64_t *row_stride);
+/* agent, block count, state (1 = offloaded, 2 = uploaded) of a live handle */
+tc_status tc_handle_info(tc_pool *p, tc_handle h, int32_t *agent, int64_t *n, int32_t *state);
+/* Host pointer to the pinned copy of block i of an offloaded handle, layout [L][2][C] (valid after tc_wait). */
+tc_status tc_handle_host(tc_pool *p, tc_handle h, int64_t i, const void **host_ptr);
+tc_status tc_stats(tc_pool *p, tc_stats_t *s);
+/* Per-launch device timing (CUDA events recorded on the launching stream around every kernel / memcpy run).
+   Spans complete at tc_sync, where their durations are accumulated.  Index: 0 offload kernels, 1 upload kernels,
+   2 device-tier kernels, 3 staged D2H memcpy, 4 staged H2D memcpy.  bytes = KV payload bytes moved (n * B). */
+typedef struct tc_timing_t {
+    double ms[5];
+    int64_t count[5];
+    int64_t bytes[5];
+} tc_timing_t;
+/* enable != 0 turns span recording on (off by default: zero overhead).  If out != NULL it receives the totals
+   accumulated since the previous call, which are then reset. */
+tc_status tc_timing(tc_pool *p, int32_t enable, tc_timing_t *out);
+const char *tc_strerror(tc_status s);
+const char *tc_last_error(tc_pool *p);
+
+/* ---- device tier (staged halves; NEXT-2 building block) ---------------------------------------------------- */
+/* Gather blocks ids[0..n) into a contiguous device buffer dst[n][L][2][C] (the HBM-bound KG1 kernel), or scatter
+   src[n][L][2][C] into blocks ids[0..n) (KS1), on `cuda_stream` (NULL = the offload stream).  No allocator or
+   table change: the caller owns the ids' meaning.  dst/src: device (or peer-mapped) pointers, 16-byte aligned. */
+tc_status tc_gather_dev(tc_pool *p, const int32_t *ids, int64_t n, void *dst_dev, void *cuda_stream);
+tc_status tc_scatter_dev(tc_pool *p, const void *src_dev, const int32_t *ids, int64_t n, void *cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOKENCAKE_H */

@@ -1,0 +1,343 @@
+"""B200-native Tokencake Time-Scheduler hot path (arXiv 2510.18586): paged KV-block offload / predictive upload.
+
+Thin ctypes binding over the C ABI in ``include/tokencake.h`` (``libtokencake.so``, built in-tree by
+``paper_2510_18586_b200/build.py``).  Argument marshalling only: every step of the path — admission, allocation,
+the gather/scatter kernels, the fused block-table remap, completion — runs in the library.  PyTorch is used only to
+own device memory (the KV pool and block table tensors) and to name streams.
+
+There is no fallback: if the shared library is missing or fails to load, importing this package raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import build as _build
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtokencake.so")
+
+OK, E_INVAL, E_NOBLOCKS, E_NOHOST, E_HANDLE, E_BUSY, E_CUDA, E_OOM, E_NODEV = 0, -1, -2, -3, -4, -5, -6, -7, -8
+FP16, BF16 = 0, 1
+XFER_AUTO, XFER_DIRECT, XFER_STAGED = 0, 1, 2
+DTYPES = {"fp16": FP16, "bf16": BF16}
+
+SYMBOLS = [
+    "tc_pool_desc_init", "tc_pool_create", "tc_pool_create_ex", "tc_pool_destroy", "tc_pool_kv",
+    "tc_set_compute_stream", "tc_streams", "tc_set_xfer_mode", "tc_fill_kv", "tc_partition_reserve",
+    "tc_agent_add", "tc_alloc", "tc_agent_free", "tc_offload", "tc_upload", "tc_offload_batch", "tc_upload_batch",
+    "tc_query", "tc_wait", "tc_stream_wait", "tc_sync", "tc_block_table", "tc_block_table_dev", "tc_handle_info",
+    "tc_handle_host", "tc_stats", "tc_timing", "tc_strerror", "tc_last_error", "tc_gather_dev", "tc_scatter_dev",
+]
+
+
+class TcError(RuntimeError):
+    def __init__(self, status: int, msg: str = ""):
+        super().__init__(f"tokencake status {status}: {msg}")
+        self.status = status
+
+
+class PoolDesc(ctypes.Structure):
+    _fields_ = [
+        ("layers", ctypes.c_int32), ("kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+        ("block_tokens", ctypes.c_int32), ("dtype", ctypes.c_int32), ("n_blocks", ctypes.c_int64),
+        ("device", ctypes.c_int32), ("shard_rank", ctypes.c_int32), ("shard_world", ctypes.c_int32),
+        ("host_slots", ctypes.c_int64), ("n_classes", ctypes.c_int32), ("max_agents", ctypes.c_int32),
+        ("max_blocks_per_agent", ctypes.c_int32), ("kv_dev", ctypes.c_void_p), ("table_dev", ctypes.c_void_p),
+        ("xfer_d2h", ctypes.c_int32), ("xfer_h2d", ctypes.c_int32), ("staging_bytes", ctypes.c_int64),
+        ("desc_bytes", ctypes.c_int64),
+    ]
+
+
+class Timing(ctypes.Structure):
+    _fields_ = [("ms", ctypes.c_double * 5), ("count", ctypes.c_int64 * 5), ("bytes", ctypes.c_int64 * 5)]
+
+
+TIMING_KINDS = ("offload_kernel", "upload_kernel", "device_kernel", "memcpy_d2h", "memcpy_h2d")
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("n_blocks", ctypes.c_int64), ("free_blocks", ctypes.c_int64), ("alloc_blocks", ctypes.c_int64),
+        ("pending_blocks", ctypes.c_int64), ("host_slots", ctypes.c_int64), ("host_free", ctypes.c_int64),
+        ("host_used", ctypes.c_int64), ("host_released", ctypes.c_int64), ("chunk_bytes", ctypes.c_int64),
+        ("block_bytes", ctypes.c_int64), ("n_classes", ctypes.c_int32), ("n_agents", ctypes.c_int32),
+        ("reserved", ctypes.c_int64 * 64), ("claimed", ctypes.c_int64 * 64), ("live_handles", ctypes.c_int64),
+        ("kernel_launches", ctypes.c_int64), ("memcpy_calls", ctypes.c_int64), ("bytes_d2h", ctypes.c_int64),
+        ("bytes_h2d", ctypes.c_int64), ("xfer_d2h", ctypes.c_int32), ("xfer_h2d", ctypes.c_int32),
+    ]
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH) or _build.stale():
+        _build.build()
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I32, I64, U64, VP = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_void_p
+    PI32, PI64, PU64 = ctypes.POINTER(I32), ctypes.POINTER(I64), ctypes.POINTER(U64)
+    sig = {
+        "tc_pool_desc_init": (None, [ctypes.POINTER(PoolDesc), I32, I32, I32, I32, I32, I64]),
+        "tc_pool_create": (I32, [I32, I32, I32, I32, I32, I64, ctypes.POINTER(P)]),
+        "tc_pool_create_ex": (I32, [ctypes.POINTER(PoolDesc), ctypes.POINTER(P)]),
+        "tc_pool_destroy": (None, [P]),
+        "tc_pool_kv": (I32, [P, ctypes.POINTER(VP), PI64]),
+        "tc_set_compute_stream": (I32, [P, VP]),
+        "tc_streams": (I32, [P, ctypes.POINTER(VP), ctypes.POINTER(VP)]),
+        "tc_set_xfer_mode": (I32, [P, I32, I32]),
+        "tc_fill_kv": (I32, [P, U64]),
+        "tc_partition_reserve": (I32, [P, I32, I64]),
+        "tc_agent_add": (I32, [P, I32, I32]),
+        "tc_alloc": (I32, [P, I32, I64, PI32]),
+        "tc_agent_free": (I32, [P, I32]),
+        "tc_offload": (I32, [P, I32, PI32, I64, PU64]),
+        "tc_upload": (I32, [P, U64, PI32]),
+        "tc_offload_batch": (I32, [P, I32, PI32, PI64, PI32, PU64]),
+        "tc_upload_batch": (I32, [P, I32, PU64, PI64, PI32]),
+        "tc_query": (I32, [P, U64]),
+        "tc_wait": (I32, [P, U64]),
+        "tc_stream_wait": (I32, [P, U64, VP]),
+        "tc_sync": (I32, [P]),
+        "tc_block_table": (I32, [P, I32, PI32, I64, PI64]),
+        "tc_block_table_dev": (I32, [P, ctypes.POINTER(PI32), PI64]),
+        "tc_handle_info": (I32, [P, U64, PI32, PI64, PI32]),
+        "tc_handle_host": (I32, [P, U64, I64, ctypes.POINTER(VP)]),
+        "tc_stats": (I32, [P, ctypes.POINTER(Stats)]),
+        "tc_timing": (I32, [P, I32, ctypes.POINTER(Timing)]),
+        "tc_strerror": (ctypes.c_char_p, [I32]),
+        "tc_last_error": (ctypes.c_char_p, [P]),
+        "tc_gather_dev": (I32, [P, PI32, I64, VP, VP]),
+        "tc_scatter_dev": (I32, [P, VP, PI32, I64, VP]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+def _ptr(a: np.ndarray, ct):
+    return a.ctypes.data_as(ctypes.POINTER(ct))
+
+
+class Pool:
+    """One paged KV pool on one CUDA device (or metadata-only with ``device=-1``), driven through the C ABI.
+
+    Method vocabulary (shared with the test replayer): reserve, agent_add, alloc, offload, upload, offload_batch,
+    upload_batch, sync, agent_free, block_table, stats, plus query / wait / stream_wait and device-tier helpers.
+    """
+
+    def __init__(self, layers: int, kv_heads: int, head_dim: int, block_tokens: int = 16, dtype: str = "bf16",
+                 n_blocks: int = 64, *, device: int = 0, shard_rank: int = 0, shard_world: int = 1,
+                 host_slots: int = 0, n_classes: int = 8, max_agents: int = 1024, max_blocks_per_agent: int = 4096,
+                 xfer_d2h: int = XFER_AUTO, xfer_h2d: int = XFER_AUTO, staging_bytes: int = 0,
+                 torch_memory: bool = True):
+        d = PoolDesc()
+        lib.tc_pool_desc_init(ctypes.byref(d), layers, kv_heads, head_dim, block_tokens, DTYPES[dtype], n_blocks)
+        d.device = device
+        d.shard_rank, d.shard_world = shard_rank, shard_world
+        d.host_slots = host_slots
+        d.n_classes, d.max_agents, d.max_blocks_per_agent = n_classes, max_agents, max_blocks_per_agent
+        d.xfer_d2h, d.xfer_h2d = xfer_d2h, xfer_h2d
+        d.staging_bytes = staging_bytes
+        self._keep = []
+        self.device = device
+        self.meta_only = device < 0
+        if not self.meta_only and torch_memory:
+            import torch   # device memory is owned by PyTorch (plumbing), the pointers are handed to the library
+            hl = kv_heads // shard_world
+            kv_bytes = layers * 2 * n_blocks * block_tokens * hl * head_dim * 2
+            kv = torch.empty(kv_bytes, dtype=torch.uint8, device=f"cuda:{device}")
+            tab = torch.empty(max_agents * max_blocks_per_agent, dtype=torch.int32, device=f"cuda:{device}")
+            torch.cuda.synchronize(device)
+            d.kv_dev, d.table_dev = kv.data_ptr(), tab.data_ptr()
+            self._keep = [kv, tab]
+        h = ctypes.c_void_p()
+        self._check(lib.tc_pool_create_ex(ctypes.byref(d), ctypes.byref(h)), None)
+        self._h = h
+        self.desc = d
+        s = self.stats()
+        self.chunk_bytes, self.block_bytes = s["chunk_bytes"], s["block_bytes"]
+        self.L, self.H, self.D, self.T = layers, kv_heads, head_dim, block_tokens
+        self.Hl = kv_heads // shard_world
+        self.N = n_blocks
+        self.max_bpa = max_blocks_per_agent
+
+    # ------------------------------------------------------------------ plumbing
+    def _check(self, st: int, h=None):
+        if st != OK:
+            msg = lib.tc_strerror(st).decode()
+            if h is not None or getattr(self, "_h", None) is not None:
+                le = lib.tc_last_error(h if h is not None else self._h)
+                if le:
+                    msg += f" ({le.decode()})"
+            raise TcError(st, msg)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.tc_pool_destroy(self._h)
+            self._h = None
+        self._keep = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    # ------------------------------------------------------------------ vocabulary
+    def reserve(self, cls: int, n: int):
+        self._check(lib.tc_partition_reserve(self._h, cls, n))
+
+    def agent_add(self, agent: int, cls: int):
+        self._check(lib.tc_agent_add(self._h, agent, cls))
+
+    def alloc(self, agent: int, n: int) -> list:
+        out = np.empty(max(n, 1), dtype=np.int32)
+        self._check(lib.tc_alloc(self._h, agent, n, _ptr(out, ctypes.c_int32)))
+        return out[:n].tolist()
+
+    def agent_free(self, agent: int):
+        self._check(lib.tc_agent_free(self._h, agent))
+
+    def offload(self, agent: int, ids) -> int:
+        a = _i32(ids)
+        h = ctypes.c_uint64()
+        self._check(lib.tc_offload(self._h, agent, _ptr(a, ctypes.c_int32), a.size, ctypes.byref(h)))
+        return h.value
+
+    def upload(self, h: int) -> list:
+        agent, n, state = self.handle_info(h) if h else (0, 1, 0)
+        out = np.empty(max(n, 1), dtype=np.int32)
+        self._check(lib.tc_upload(self._h, h, _ptr(out, ctypes.c_int32)))
+        return out[:n].tolist()
+
+    def offload_batch(self, items) -> list:
+        agents = _i32([a for a, _ in items])
+        offs = np.zeros(len(items) + 1, dtype=np.int64)
+        offs[1:] = np.cumsum([len(ids) for _, ids in items])
+        ids = _i32([b for _, x in items for b in x]) if offs[-1] else np.zeros(1, np.int32)
+        out = np.zeros(max(len(items), 1), dtype=np.uint64)
+        self._check(lib.tc_offload_batch(self._h, len(items), _ptr(agents, ctypes.c_int32),
+                                         _ptr(offs, ctypes.c_int64), _ptr(ids, ctypes.c_int32),
+                                         _ptr(out, ctypes.c_uint64)))
+        return [int(x) for x in out[:len(items)]]
+
+    def offload_batch_arrays(self, agents: np.ndarray, offsets: np.ndarray, ids: np.ndarray) -> np.ndarray:
+        """Zero-copy batch entry for prebuilt int32/int64 arrays (bench hot loop)."""
+        out = np.zeros(len(agents), dtype=np.uint64)
+        self._check(lib.tc_offload_batch(self._h, len(agents), _ptr(agents, ctypes.c_int32),
+                                         _ptr(offsets, ctypes.c_int64), _ptr(ids, ctypes.c_int32),
+                                         _ptr(out, ctypes.c_uint64)))
+        return out
+
+    def upload_batch(self, hs) -> list:
+        hs_a = np.ascontiguousarray(np.asarray(hs, dtype=np.uint64))
+        sizes = []
+        for h in hs:
+            try:
+                sizes.append(self.handle_info(int(h))[1])
+            except TcError:
+                sizes.append(0)
+        offs = np.zeros(len(hs) + 1, dtype=np.int64)
+        offs[1:] = np.cumsum(sizes)
+        out = np.empty(max(int(offs[-1]), 1), dtype=np.int32)
+        self._check(lib.tc_upload_batch(self._h, len(hs), _ptr(hs_a, ctypes.c_uint64), _ptr(offs, ctypes.c_int64),
+                                        _ptr(out, ctypes.c_int32)))
+        return [out[offs[k]:offs[k + 1]].tolist() for k in range(len(hs))]
+
+    def upload_batch_arrays(self, hs: np.ndarray, offsets: np.ndarray, out: np.ndarray) -> np.ndarray:
+        self._check(lib.tc_upload_batch(self._h, len(hs), _ptr(hs, ctypes.c_uint64), _ptr(offsets, ctypes.c_int64),
+                                        _ptr(out, ctypes.c_int32)))
+        return out
+
+    def sync(self):
+        self._check(lib.tc_sync(self._h))
+
+    def query(self, h: int) -> bool:
+        st = lib.tc_query(self._h, h)
+        if st == E_BUSY:
+            return False
+        self._check(st)
+        return True
+
+    def wait(self, h: int):
+        self._check(lib.tc_wait(self._h, h))
+
+    def stream_wait(self, h: int, stream_ptr: int):
+        self._check(lib.tc_stream_wait(self._h, h, stream_ptr))
+
+    def block_table(self, agent: int) -> list:
+        n = ctypes.c_int64()
+        self._check(lib.tc_block_table(self._h, agent, None, 0, ctypes.byref(n)))
+        out = np.empty(max(n.value, 1), dtype=np.int32)
+        self._check(lib.tc_block_table(self._h, agent, _ptr(out, ctypes.c_int32), out.size, ctypes.byref(n)))
+        return out[:n.value].tolist()
+
+    def handle_info(self, h: int):
+        a, n, s = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int32()
+        self._check(lib.tc_handle_info(self._h, h, ctypes.byref(a), ctypes.byref(n), ctypes.byref(s)))
+        return a.value, n.value, s.value
+
+    def handle_host_bytes(self, h: int, i: int) -> np.ndarray:
+        """Copy of the pinned host image [L][2][C] of block i of an offloaded handle (call wait() first)."""
+        p = ctypes.c_void_p()
+        self._check(lib.tc_handle_host(self._h, h, i, ctypes.byref(p)))
+        buf = (ctypes.c_uint8 * self.block_bytes).from_address(p.value)
+        return np.frombuffer(buf, dtype=np.uint8).copy().reshape(self.L, 2, self.chunk_bytes)
+
+    def stats(self) -> dict:
+        s = Stats()
+        self._check(lib.tc_stats(self._h, ctypes.byref(s)))
+        d = {k: getattr(s, k) for k, _ in Stats._fields_ if k not in ("reserved", "claimed")}
+        d["reserved"] = list(s.reserved[:s.n_classes])
+        d["claimed"] = list(s.claimed[:s.n_classes])
+        d["free"], d["alloc"], d["pending"] = s.free_blocks, s.alloc_blocks, s.pending_blocks
+        return d
+
+    def timing(self, enable: bool = True) -> dict:
+        """Enable/disable per-launch event timing; returns {kind: (ms, count, bytes)} accumulated since last call."""
+        t = Timing()
+        self._check(lib.tc_timing(self._h, 1 if enable else 0, ctypes.byref(t)))
+        return {k: (t.ms[i], t.count[i], t.bytes[i]) for i, k in enumerate(TIMING_KINDS)}
+
+    def streams(self):
+        up, off = ctypes.c_void_p(), ctypes.c_void_p()
+        self._check(lib.tc_streams(self._h, ctypes.byref(up), ctypes.byref(off)))
+        return up.value, off.value
+
+    def set_compute_stream(self, stream_ptr: int | None):
+        self._check(lib.tc_set_compute_stream(self._h, stream_ptr))
+
+    def set_xfer_mode(self, d2h: int, h2d: int):
+        self._check(lib.tc_set_xfer_mode(self._h, d2h, h2d))
+
+    def fill(self, seed: int):
+        self._check(lib.tc_fill_kv(self._h, seed))
+
+    def kv_ptr(self) -> int:
+        p, c = ctypes.c_void_p(), ctypes.c_int64()
+        self._check(lib.tc_pool_kv(self._h, ctypes.byref(p), ctypes.byref(c)))
+        return p.value
+
+    def kv_tensor(self):
+        """The KV pool as a torch uint8 tensor view [L][2][N][C] (torch-owned memory)."""
+        return self._keep[0].view(self.L, 2, self.N, self.chunk_bytes)
+
+    def table_tensor(self):
+        return self._keep[1].view(-1, self.max_bpa)
+
+    def gather_dev(self, ids, dst_ptr: int, stream_ptr: int | None = None):
+        a = _i32(ids)
+        self._check(lib.tc_gather_dev(self._h, _ptr(a, ctypes.c_int32), a.size, dst_ptr, stream_ptr))
+
+    def scatter_dev(self, src_ptr: int, ids, stream_ptr: int | None = None):
+        a = _i32(ids)
+        self._check(lib.tc_scatter_dev(self._h, src_ptr, _ptr(a, ctypes.c_int32), a.size, stream_ptr))

@@ -1,0 +1,140 @@
+// sm_100a gather / scatter kernels of the Tokencake offload/upload hot path, and the synthetic-content fill kernel.
+//
+// Data movement only — no tensor cores (no contraction anywhere on this path).  One warp copies one
+// (block, layer, K|V) chunk of C contiguous bytes with 16-byte vector loads/stores, U loads in flight per lane before
+// the matching stores (Little's law against HBM / host-link latency).  Each CTA owns a contiguous range of chunks,
+// stages that range's descriptors in shared memory once (one host-link round trip when the descriptors sit in mapped
+// pinned memory), and the warp that copies chunk 0 of a block performs the fused block-table epilogue
+// (P:649 location flag / remap).
+#include "kernels.cuh"
+
+namespace tc {
+namespace {
+
+constexpr int kUnroll = 8;
+
+__device__ __forceinline__ int4 ld_stream(const int4 *p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ void st_stream(int4 *p, const int4 &v) {
+    asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+
+// Copy nv int4 vectors; the warp's 32 lanes cover 512 contiguous bytes per step.
+__device__ __forceinline__ void warp_copy(int4 *__restrict__ dst, const int4 *__restrict__ src, int64_t nv, int lane) {
+    int64_t v = lane;
+    for (; v + 32 * (kUnroll - 1) < nv; v += 32 * kUnroll) {
+        int4 r[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) r[u] = ld_stream(src + v + 32 * u);
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) st_stream(dst + v + 32 * u, r[u]);
+    }
+    for (; v < nv; v += 32) st_stream(dst + v, ld_stream(src + v));
+}
+
+template <bool kGather>
+__global__ void __launch_bounds__(256) k_xfer(const XferDesc *__restrict__ desc, int64_t n, XferGeom g,
+                                              char *__restrict__ kv, int32_t *__restrict__ table,
+                                              int64_t chunks_per_cta) {
+    extern __shared__ XferDesc sdesc[];
+    const int64_t M = n * g.two_l;
+    const int64_t j0 = (int64_t)blockIdx.x * chunks_per_cta;
+    if (j0 >= M) return;
+    const int64_t j1 = min(M, j0 + chunks_per_cta);
+    const int64_t i0 = j0 / g.two_l;
+    const int nb = (int)((j1 - 1) / g.two_l - i0 + 1);
+    {
+        const int4 *s = reinterpret_cast<const int4 *>(desc + i0);
+        int4 *d = reinterpret_cast<int4 *>(sdesc);
+        for (int k = threadIdx.x; k < nb; k += blockDim.x) d[k] = s[k];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    const int64_t nv = g.chunk >> 4;
+    for (int64_t j = j0 + warp; j < j1; j += nwarps) {
+        const int64_t i = j / g.two_l;
+        const int64_t lk = j - i * g.two_l;
+        const XferDesc d = sdesc[i - i0];
+        char *pool_chunk = kv + (lk * g.n_pool + d.blk) * g.chunk;
+        char *ext_chunk = reinterpret_cast<char *>(d.ext) + lk * g.chunk;
+        if (kGather)
+            warp_copy(reinterpret_cast<int4 *>(ext_chunk), reinterpret_cast<const int4 *>(pool_chunk), nv, lane);
+        else
+            warp_copy(reinterpret_cast<int4 *>(pool_chunk), reinterpret_cast<const int4 *>(ext_chunk), nv, lane);
+        if (lk == 0 && lane == 0 && d.tab >= 0) table[d.tab] = kGather ? -1 : d.blk;
+    }
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// One CTA per (layer*2+kv, block) chunk (grid-stride); words inside a chunk in [T][Hl][wpr] order.
+__global__ void k_fill(uint64_t *__restrict__ kv, int64_t n_chunks, int64_t n_pool, int32_t T, int32_t H,
+                       int32_t Hl, int32_t rank, int32_t wpr, uint64_t seedk) {
+    const int32_t cw = T * Hl * wpr;  // words per chunk
+    for (int64_t q = blockIdx.x; q < n_chunks; q += gridDim.x) {
+        const uint64_t base = (uint64_t)q * (uint64_t)T;   // ((lk*N + b) * T) in the unsharded index
+        uint64_t *dst = kv + q * (int64_t)cw;
+        for (int32_t w = threadIdx.x; w < cw; w += blockDim.x) {
+            const int32_t ww = w % wpr;
+            const int32_t r = w / wpr;
+            const int32_t hl = r % Hl;
+            const int32_t t = r / Hl;
+            const uint64_t widx = ((base + t) * (uint64_t)H + (uint64_t)(rank * Hl + hl)) * (uint64_t)wpr + ww;
+            dst[w] = splitmix64(widx + seedk);
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_xfer(bool gather, const XferDesc *desc, int64_t n, const XferGeom &g, void *kv, int32_t *table,
+                        int ctas, int threads, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t M = n * g.two_l;
+    if (threads <= 0 || threads > 256) threads = 256;
+    if (ctas <= 0) ctas = 148 * 4;
+    const int64_t nwarps = threads / 32;
+    int64_t grid = std::min<int64_t>(ctas, (M + nwarps - 1) / nwarps);
+    if (grid < 1) grid = 1;
+    const int64_t cpc = (M + grid - 1) / grid;
+    grid = (M + cpc - 1) / cpc;
+    const int64_t max_nb = cpc / g.two_l + 2;
+    const size_t smem = (size_t)max_nb * sizeof(XferDesc);
+    if (smem > 48 * 1024) {
+        auto fn = gather ? k_xfer<true> : k_xfer<false>;
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    if (gather)
+        k_xfer<true><<<(unsigned)grid, threads, smem, s>>>(desc, n, g, static_cast<char *>(kv), table, cpc);
+    else
+        k_xfer<false><<<(unsigned)grid, threads, smem, s>>>(desc, n, g, static_cast<char *>(kv), table, cpc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill(void *kv, int64_t n_pool, int32_t L, int32_t T, int32_t H, int32_t Hl, int32_t rank,
+                        int32_t D, uint64_t seed, cudaStream_t s) {
+    const int32_t wpr = D * 2 / 8;
+    const int64_t n_chunks = (int64_t)L * 2 * n_pool;
+    const uint64_t seedk = seed * 0xD1B54A32D192ED03ull;
+    const int64_t grid = std::min<int64_t>(n_chunks, 148 * 16);
+    k_fill<<<(unsigned)grid, 256, 0, s>>>(static_cast<uint64_t *>(kv), n_chunks, n_pool, T, H, Hl, rank, wpr, seedk);
+    return cudaGetLastError();
+}
+
+}  // namespace tc

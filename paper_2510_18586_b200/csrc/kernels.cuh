@@ -1,0 +1,36 @@
+// Internal launch interface of the sm_100a kernels (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tc {
+
+// One transfer descriptor per block (16 B).  `ext` is the device-visible address of the block's contiguous
+// [L][2][C] image outside the pool: a mapped pinned host slot (DIRECT), a device staging slot (STAGED) or a caller
+// buffer (device tier).  `tab` is the flat index of the block-table entry the fused epilogue rewrites
+// (agent * row_stride + pos), or -1 for none.
+struct XferDesc {
+    int32_t blk;
+    int32_t tab;
+    uint64_t ext;
+};
+static_assert(sizeof(XferDesc) == 16, "XferDesc must be 16 bytes");
+
+struct XferGeom {
+    int64_t n_pool;      // N
+    int64_t chunk;       // C bytes (multiple of 16)
+    int32_t two_l;       // 2L chunks per block
+};
+
+// gather: ext[i] + lk*C  <-  kv + (lk*N + blk_i)*C      (a3: offload; epilogue table[tab_i] = -1)
+// scatter: kv + (lk*N + blk_i)*C  <-  ext[i] + lk*C     (a6: upload; epilogue table[tab_i] = blk_i)
+// `desc` may live in mapped pinned memory.  ctas <= 0 selects the default grid.
+cudaError_t launch_xfer(bool gather, const XferDesc *desc, int64_t n, const XferGeom &g, void *kv, int32_t *table,
+                        int ctas, int threads, cudaStream_t s);
+
+// Synthetic content: word w of the unsharded [L][2][N][T][H][D] pool =
+// splitmix64(w + seed * 0xD1B54A32D192ED03); this shard holds heads [rank*Hl, (rank+1)*Hl).
+cudaError_t launch_fill(void *kv, int64_t n_pool, int32_t L, int32_t T, int32_t H, int32_t Hl, int32_t rank,
+                        int32_t D, uint64_t seed, cudaStream_t s);
+
+}  // namespace tc

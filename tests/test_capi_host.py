@@ -1,0 +1,129 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol include/tokencake.h declares, and its host
+logic (allocator, partitions, host-slot buffer, handles, tables, batch semantics, error statuses) replays every
+script identically to the oracle.  Uses metadata-only pools (device = -1): bookkeeping without KV storage — no data
+is produced or compared here (that is the -m gpu parity suite)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2510_18586_b200 as tcb
+from oracle import OraclePool, ProvStore
+from workloads.configs import CONFIGS
+from workloads.replay import Replayer
+from workloads.scripts import N_CLASSES, build_script, c1_worked_example, fuzz_script
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "tokencake.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(tc_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(tcb.LIB_PATH)
+    syms = header_symbols()
+    assert len(syms) >= 29
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(tcb.SYMBOLS)
+
+
+def test_strerror_and_status_codes():
+    for st in (0, -1, -2, -3, -4, -5, -6, -7, -8):
+        assert tcb.lib.tc_strerror(st)
+    assert tcb.lib.tc_strerror(0).decode() == "ok"
+
+
+def meta_pool(N, S, ncls=N_CLASSES, max_bpa=4096, L=1, H=2, D=64):
+    return tcb.Pool(L, H, D, 16, "fp16", N, device=-1, host_slots=S, n_classes=ncls, max_agents=1024,
+                    max_blocks_per_agent=max_bpa)
+
+
+def stats_view(s):
+    return {k: s[k] for k in ("free", "alloc", "pending", "host_free", "host_used", "reserved", "claimed")}
+
+
+def replay_both(ops, N, S, ncls=N_CLASSES, max_bpa=4096):
+    o = OraclePool(N, S, n_classes=ncls, max_agents=1024, max_blocks_per_agent=max_bpa, store=ProvStore(N, S))
+    c = meta_pool(N, S, ncls, max_bpa)
+    ro, rc = Replayer(o), Replayer(c)
+    for i, op in enumerate(ops):
+        a, b = ro.step(op), rc.step(op)
+        assert a == b, (i, op, a, b)
+        if op[0] in ("sync", "upload_batch", "offload_batch"):
+            assert stats_view(o.stats()) == stats_view(c.stats()), (i, op)
+    for ag in o.agents:
+        assert o.block_table(ag) == c.block_table(ag)
+    assert stats_view(o.stats()) == stats_view(c.stats())
+    return o, c
+
+
+def test_c1_worked_example_through_capi():
+    o, c = replay_both(c1_worked_example(), 64, 16)
+    assert c.block_table(0) == [6, 8, 10, 12, 14, 20, 21, 22]
+    s = c.stats()
+    assert (s["free"], s["alloc"], s["pending"]) == (41, 23, 0)
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_fuzz_scripts_match_oracle(seed):
+    rng = np.random.default_rng(seed)
+    N = int(rng.choice([8, 24, 64]))
+    S = int(rng.choice([4, 10, 32]))
+    ops = fuzz_script(seed, n_ops=150, n_agents=3, n_classes=2, N=N, max_alloc=int(rng.choice([2, 6, 12])))
+    replay_both(ops, N, S, ncls=2, max_bpa=int(rng.choice([8, 4096])))
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_config_scripts_match_oracle_full_size(name):
+    """Full-size (N, agents, sizes) scripts of every config: identical ids, handles, tables and counters."""
+    cfg = CONFIGS[name]
+    cycles = 6 if name != "c1" else 4
+    ops = build_script(cfg, cycles) if name != "c1" else c1_worked_example() + fuzz_script(1, 80)
+    replay_both(ops, cfg.N, cfg.host_slots(), max_bpa=cfg.max_blocks_per_agent)
+
+
+def test_batch_all_or_nothing_and_first_failure_status():
+    c = meta_pool(16, 6, ncls=2)
+    c.agent_add(0, 0); c.agent_add(1, 1)
+    c.alloc(0, 4); c.alloc(1, 4)
+    before = (c.block_table(0), c.block_table(1), stats_view(c.stats()))
+    # item 0 needs 4 slots, item 1 needs 4 more: cumulative NOHOST at item 1 -> nothing offloaded
+    with pytest.raises(tcb.TcError) as e:
+        c.offload_batch([(0, c.block_table(0)), (1, c.block_table(1))])
+    assert e.value.status == tcb.E_NOHOST
+    assert before == (c.block_table(0), c.block_table(1), stats_view(c.stats()))
+    # item 0 NOHOST? no: item 0 invalid (block of agent 1) -> INVAL even though item 1 would be NOHOST
+    with pytest.raises(tcb.TcError) as e:
+        c.offload_batch([(0, c.block_table(1)[:1]), (1, c.block_table(1))])
+    assert e.value.status == tcb.E_INVAL
+    h = c.offload_batch([(0, c.block_table(0)[:2]), (1, c.block_table(1)[:2])])
+    assert h == [1, 2]
+    with pytest.raises(tcb.TcError) as e:
+        c.upload_batch([1, 1])
+    assert e.value.status == tcb.E_HANDLE
+    assert c.upload_batch([2, 1]) == [[8, 9], [10, 11]]
+
+
+def test_metadata_only_pool_refuses_data_ops():
+    c = meta_pool(8, 4)
+    with pytest.raises(tcb.TcError) as e:
+        c.fill(1)
+    assert e.value.status == tcb.E_NODEV
+    with pytest.raises(tcb.TcError) as e:
+        c.kv_ptr()
+    assert e.value.status == tcb.E_NODEV
+
+
+def test_create_rejects_bad_geometry():
+    for kw in (dict(L=0), dict(H=3), dict(D=2)):
+        args = dict(L=1, H=2, D=64)
+        args.update(kw)
+        with pytest.raises(tcb.TcError) as e:
+            tcb.Pool(args["L"], args["H"], args["D"], 16, "fp16", 8, device=-1, shard_world=2 if kw.get("H") else 1)
+        assert e.value.status == tcb.E_INVAL

@@ -1,0 +1,206 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, byte for byte, on the same seeded inputs.
+
+* small pools (C1 and fuzz scripts, several geometries with ragged chunk counts): the whole device pool, every live
+  handle's pinned host image, every block table (host mirror and device table) and all counters are compared
+  after every sync, in both transfer modes (DIRECT mapped-host kernels, STAGED device ring + copy engine);
+* full BASELINE sizes (C2..C5 shard, in the launch configuration bench.py times): tables and counters in full, KV
+  bytes on sampled (layer, K|V, block) chunks against the generator at the oracle's provenance;
+* the synthetic-content fill kernel against workloads/content.py; the device tier against numpy.take.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+import paper_2510_18586_b200 as tcb  # noqa: E402
+from oracle import BytesStore, OraclePool, ProvStore  # noqa: E402
+from oracle.pool import OFFLOADED  # noqa: E402
+from workloads import content  # noqa: E402
+from workloads.configs import CONFIGS  # noqa: E402
+from workloads.replay import Replayer  # noqa: E402
+from workloads.scripts import N_CLASSES, build_script, c1_worked_example, fuzz_script  # noqa: E402
+
+MODES = {"direct": (tcb.XFER_DIRECT, tcb.XFER_DIRECT), "staged": (tcb.XFER_STAGED, tcb.XFER_STAGED),
+         "mixed": (tcb.XFER_DIRECT, tcb.XFER_STAGED)}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def dev_pool(L, H, D, N, S, mode="direct", ncls=N_CLASSES, max_bpa=4096, seed=1, rank=0, world=1, staging=0,
+             dtype="bf16", T=16):
+    d2h, h2d = MODES[mode]
+    p = tcb.Pool(L, H, D, T, dtype, N, device=0, shard_rank=rank, shard_world=world, host_slots=S, n_classes=ncls,
+                 max_agents=1024, max_blocks_per_agent=max_bpa, xfer_d2h=d2h, xfer_h2d=h2d, staging_bytes=staging)
+    p.fill(seed)
+    return p
+
+
+def compare_full(o: OraclePool, c: tcb.Pool, where=""):
+    kv = c.kv_tensor().cpu().numpy()
+    assert np.array_equal(kv, o.store.pool), f"pool bytes differ {where}"
+    for a in o.agents:
+        assert o.block_table(a) == c.block_table(a), (where, a)
+    tab = c.table_tensor().cpu().numpy()
+    for a, ag in o.agents.items():
+        assert tab[a, :len(ag.table)].tolist() == ag.table, (where, a)
+    so, sc = o.stats(), c.stats()
+    for k in ("free", "alloc", "pending", "host_free", "host_used", "reserved", "claimed"):
+        assert so[k] == sc[k], (where, k)
+
+
+def compare_live_host(o: OraclePool, c: tcb.Pool, where=""):
+    for h, hd in o.handles.items():
+        if hd.state != OFFLOADED:
+            continue
+        c.wait(h)
+        for i, s in enumerate(hd.slots):
+            assert np.array_equal(c.handle_host_bytes(h, i), o.store.host[s]), (where, h, i)
+
+
+def run_script(ops, L, H, D, N, S, mode, ncls=N_CLASSES, max_bpa=4096, seed=1, staging=0, T=16):
+    pool0 = content.pool_bytes(seed, L, N, T, H, D)
+    o = OraclePool(N, S, n_classes=ncls, max_agents=1024, max_blocks_per_agent=max_bpa, store=BytesStore(pool0, S))
+    c = dev_pool(L, H, D, N, S, mode, ncls, max_bpa, seed, staging=staging, T=T)
+    assert np.array_equal(c.kv_tensor().cpu().numpy(), pool0), "fill kernel != content generator"
+    ro, rc = Replayer(o), Replayer(c)
+    for i, op in enumerate(ops):
+        a, b = ro.step(op), rc.step(op)
+        assert a == b, (i, op, a, b)
+        if op[0] in ("offload", "offload_batch") and a[0] == 0:
+            compare_live_host(o, c, f"op {i}")
+        if op[0] == "sync":
+            compare_full(o, c, f"op {i}")
+    c.sync()
+    compare_full(o, c, "end")
+    return o, c
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+def test_c1_worked_example_bytes(mode):
+    o, c = run_script(c1_worked_example(), 1, 2, 64, 64, 16, mode)
+    assert c.block_table(0) == [6, 8, 10, 12, 14, 20, 21, 22]
+
+
+GEOMS = [  # (L, H, D, N, S, T): ragged chunk counts vs CTA ranges, 4 KiB .. 32 KiB chunks
+    (1, 2, 64, 64, 16, 16),
+    (3, 2, 64, 50, 20, 16),
+    (5, 4, 128, 40, 24, 16),
+    (2, 8, 128, 33, 12, 16),
+    (7, 1, 8, 29, 9, 3),      # C = 48 B: sub-warp chunks (ragged tail inside a chunk)
+]
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+@pytest.mark.parametrize("gi", range(len(GEOMS)))
+def test_fuzz_scripts_bytes(mode, gi):
+    L, H, D, N, S, T = GEOMS[gi]
+    for seed in range(3):
+        ops = fuzz_script(seed + 10 * gi, n_ops=90, n_agents=3, n_classes=2, N=N)
+        run_script(ops, L, H, D, N, S, mode, ncls=2, seed=seed + 1, staging=(3 * 2 * L * T * H * D * 2), T=T)
+
+
+def test_fill_kernel_matches_generator_sharded():
+    L, H, D, N = 3, 8, 128, 20
+    full = content.pool_bytes(5, L, N, 16, H, D)
+    for world in (1, 2, 4, 8):
+        for rank in range(world):
+            c = dev_pool(L, H, D, N, 4, rank=rank, world=world, seed=5)
+            got = c.kv_tensor().cpu().numpy().reshape(L, 2, N, 16, H // world, D * 2)
+            exp = full.reshape(L, 2, N, 16, H, D * 2)[:, :, :, :, rank * H // world:(rank + 1) * H // world]
+            assert np.array_equal(got, exp), (world, rank)
+            c.close()
+
+
+def test_device_tier_equals_numpy_take():
+    L, H, D, N = 4, 4, 128, 64
+    c = dev_pool(L, H, D, N, 4, seed=9)
+    pool0 = content.pool_bytes(9, L, N, 16, H, D)
+    rng = np.random.default_rng(0)
+    ids = rng.choice(N, size=23, replace=False).astype(np.int32)
+    dst = torch.empty(23 * c.block_bytes, dtype=torch.uint8, device="cuda:0")
+    c.gather_dev(ids, dst.data_ptr())
+    torch.cuda.synchronize()
+    got = dst.cpu().numpy().reshape(23, L, 2, c.chunk_bytes)
+    assert np.array_equal(got, np.take(pool0, ids, axis=2).transpose(2, 0, 1, 3))
+    tgt = rng.choice(N, size=23, replace=False).astype(np.int32)
+    c.scatter_dev(dst.data_ptr(), tgt)
+    torch.cuda.synchronize()
+    ref = pool0.copy()
+    ref[:, :, tgt] = got.transpose(1, 2, 0, 3)
+    assert np.array_equal(c.kv_tensor().cpu().numpy(), ref)
+
+
+def test_special_bit_patterns_survive_round_trip():
+    """NaN payloads, +-Inf, -0, denormals: the path is a bit copy (A14)."""
+    L, H, D, N = 1, 2, 64, 16
+    c = dev_pool(L, H, D, N, 8)
+    pat = np.array([0x7FC1, 0xFFFF, 0x7F80, 0xFF80, 0x8000, 0x0001, 0x8001, 0x7FBF], dtype=np.uint16)
+    words = np.resize(pat, c.kv_tensor().numel() // 2)
+    c.kv_tensor().copy_(torch.from_numpy(words.view(np.uint8).reshape(c.kv_tensor().shape)))
+    before = c.kv_tensor().cpu().numpy().copy()
+    c.agent_add(0, 0); c.agent_add(1, 0)
+    ids = c.alloc(0, 6)
+    c.alloc(1, 2)
+    h = c.offload(0, ids)
+    c.sync()
+    c.alloc(1, 3)
+    new = c.upload(h)
+    c.sync()
+    after = c.kv_tensor().cpu().numpy()
+    assert np.array_equal(after[:, :, new], before[:, :, ids])
+
+
+# --------------------------------------------------------------------------------------- full BASELINE sizes
+def sample_check(c: tcb.Pool, cfg, prov: np.ndarray, blocks: np.ndarray, seed: int, rank: int, world: int,
+                 rng, per_block: int = 2):
+    L = cfg.L
+    kvt = c.kv_tensor()
+    lk = rng.integers(0, 2 * L, size=(len(blocks), per_block))
+    bl = np.repeat(blocks, per_block)
+    lk = lk.reshape(-1)
+    got = kvt[torch.from_numpy(lk // 2).cuda(), torch.from_numpy(lk % 2).cuda(),
+              torch.from_numpy(bl.astype(np.int64)).cuda()].cpu().numpy()
+    for k in range(len(bl)):
+        exp = content.chunk_bytes(seed, int(lk[k] // 2), int(lk[k] % 2), int(prov[bl[k]]), cfg.N, cfg.T, cfg.H,
+                                  cfg.D, rank=rank, world=world)
+        assert np.array_equal(got[k], exp), (cfg.name, int(bl[k]), int(lk[k]))
+
+
+@pytest.mark.parametrize("name,world", [("c2", 1), ("c3", 1), ("c4", 8), ("c5", 8)])
+def test_full_size_config_parity(name, world):
+    cfg = CONFIGS[name]
+    rank = world - 1 if world > 1 else 0
+    S = cfg.host_slots()
+    ops = build_script(cfg, 8)
+    o = OraclePool(cfg.N, S, max_agents=1024, max_blocks_per_agent=cfg.max_blocks_per_agent,
+                   store=ProvStore(cfg.N, S))
+    c = tcb.Pool(cfg.L, cfg.H, cfg.D, cfg.T, cfg.dtype, cfg.N, device=0, shard_rank=rank, shard_world=world,
+                 host_slots=S, max_agents=1024, max_blocks_per_agent=cfg.max_blocks_per_agent)
+    c.fill(cfg.seed)
+    ro, rc = Replayer(o), Replayer(c)
+    touched = set()
+    for i, op in enumerate(ops):
+        a, b = ro.step(op), rc.step(op)
+        assert a == b, (i, op)
+        assert a[0] == 0, (i, op)
+        if op[0] in ("upload_batch", "upload") and a[1]:
+            for ids in (a[1] if op[0] == "upload_batch" else [a[1]]):
+                touched.update(ids)
+    c.sync()
+    tab = c.table_tensor().cpu().numpy()
+    for ag_id, ag in o.agents.items():
+        assert c.block_table(ag_id) == ag.table
+        assert tab[ag_id, :len(ag.table)].tolist() == ag.table
+    rng = np.random.default_rng(cfg.seed)
+    touched = np.array(sorted(touched), dtype=np.int64)
+    assert len(touched) > 0
+    sample_check(c, cfg, o.store.prov, touched, cfg.seed, rank, world, rng)
+    others = rng.choice(cfg.N, size=512, replace=False)
+    sample_check(c, cfg, o.store.prov, others, cfg.seed, rank, world, rng)
+    c.close()
