@@ -39,7 +39,7 @@ HBM_FALLBACK = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback (GB/s), 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=None)
@@ -183,33 +183,30 @@ def run_ours(args):
             pool.agent_free(op[1])
         elif k == "sync":
             pool.sync()
-    gen = CycleGen(cfg, agents)
-    handles = {}
+    gen = CycleGen(cfg, agents, combined=True)
+    handles, sizes = {}, {}
 
     def cycle(record=None):
-        """One scheduling cycle through the public API; returns (blocks_up, blocks_off)."""
-        cyc = gen.next_cycle()
+        """One scheduling cycle through the public API (tc_cycle: uploads then offloads, then tc_sync);
+        returns (blocks_up, blocks_off)."""
         nu = no = 0
-        for op in cyc:
-            if op[0] == "upload_batch":
+        for op in gen.next_cycle():
+            if op[0] == "cycle":
                 hs = np.array([handles.pop(a) for a in op[1]], dtype=np.uint64)
-                sizes = [pool.handle_info(int(h))[1] for h in hs]
-                offs = np.zeros(len(hs) + 1, dtype=np.int64); offs[1:] = np.cumsum(sizes)
-                out = np.empty(int(offs[-1]), dtype=np.int32)
-                pool.upload_batch_arrays(hs, offs, out)
-                nu += int(offs[-1])
-            elif op[0] == "offload_batch":
-                ags = np.array([a for a, _ in op[1]], dtype=np.int32)
+                uoff = np.zeros(len(hs) + 1, dtype=np.int64)
+                uoff[1:] = np.cumsum([sizes.pop(int(h)) for h in hs])
+                ags = np.array([a for a, _ in op[2]], dtype=np.int32)
                 tabs = [np.asarray(pool.block_table(int(a)), dtype=np.int32) for a in ags]
                 tabs = [t[t >= 0] for t in tabs]
-                offs = np.zeros(len(tabs) + 1, dtype=np.int64); offs[1:] = np.cumsum([len(t) for t in tabs])
-                ids = np.ascontiguousarray(np.concatenate(tabs))
-                if record is not None:
-                    record("pre_offload")
-                hs = pool.offload_batch_arrays(ags, offs, ids)
-                for a, h in zip(ags, hs):
+                ooff = np.zeros(len(tabs) + 1, dtype=np.int64)
+                ooff[1:] = np.cumsum([len(t) for t in tabs])
+                ids = np.ascontiguousarray(np.concatenate(tabs)) if tabs else np.zeros(1, np.int32)
+                _, out_h = pool.cycle_arrays(hs, uoff, ags, ooff, ids)
+                for a, h, t in zip(ags, out_h, tabs):
                     handles[int(a)] = int(h)
-                no += int(offs[-1])
+                    sizes[int(h)] = len(t)
+                nu += int(uoff[-1])
+                no += int(ooff[-1])
             elif op[0] == "sync":
                 if record is not None:
                     record("end")
@@ -220,6 +217,7 @@ def run_ours(args):
     up_s, off_s = pool.streams()
     ups, offs_ = torch.cuda.ExternalStream(up_s, device=dev), torch.cuda.ExternalStream(off_s, device=dev)
 
+    clocks = Clocks(local)                     # sampled from warm-up through the end of the timed region
     for _ in range(cfg.stall_cycles + 1):      # prime: get stalled agents to upload
         cycle()
     for _ in range(args.warmup):
@@ -227,11 +225,11 @@ def run_ours(args):
     pool.timing(True)
     pool.timing(True)                          # reset accumulators
     launches0 = pool.stats()["kernel_launches"]
+    memcpy0 = pool.stats()["memcpy_calls"]
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    clocks = Clocks(local)
-    dev_ms, host_ms, bytes_up, bytes_off, blocks = [], [], 0, 0, 0
+    dev_ms, host_ms, bytes_up, bytes_off, blocks, step_bytes = [], [], 0, 0, 0, []
     t_wall0 = time.perf_counter()
     for _ in range(args.steps):
         flush.zero_()                          # flush L2 between steps (outside the step's events)
@@ -252,6 +250,7 @@ def run_ours(args):
         end = max(ref.elapsed_time(ev["up1"]), ref.elapsed_time(ev["off1"]))
         dev_ms.append(end - start)
         host_ms.append((t1 - t0) * 1e3)
+        step_bytes.append((nu * B, no * B))
         bytes_up += nu * B
         bytes_off += no * B
         blocks += nu + no
@@ -291,21 +290,43 @@ def run_ours(args):
         if cnt:
             kern[k] = {"ms_total": ms, "runs": cnt, "achieved_gbs": byt / (ms * 1e-3) / 1e9}
     stats = pool.stats()
-    staged = stats["xfer_d2h"] == tcb.XFER_STAGED
     roof = None
-    if kern:
-        dom = max((k for k in kern if k.endswith("_kernel")), key=lambda k: kern[k]["ms_total"])
-        kd = kern[dom]
-        if staged:   # device-side gather/scatter: HBM-bound, read + write bytes
+    kern_only = {k: v for k, v in kern.items() if k.endswith("_kernel")}
+    if kern_only:
+        dom = max(kern_only, key=lambda k: kern_only[k]["ms_total"])
+        kd = kern_only[dom]
+        if kd["peak_key"] and stats["xfer_d2h"] == tcb.XFER_DIRECT and dom == "offload_kernel" or \
+                stats["xfer_h2d"] == tcb.XFER_DIRECT and dom == "upload_kernel":
+            pk = link[kd["peak_key"]] if link else None   # direct mapped-host kernel: bound by the host link
+            roof = {"kernel": dom + " (direct, mapped host)", "bound": "host_link", "achieved": kd["achieved_gbs"],
+                    "peak": pk, "unit": "GB/s", "frac": (kd["achieved_gbs"] / pk) if pk else None, "traffic": None,
+                    "bytes_per_launch": kd["bytes_per_launch"], "ms_per_launch": kd["ms_total"] / kd["launches"],
+                    "peak_source": "live pinned cudaMemcpyAsync 1 GiB in this run"}
+        else:                                              # staged device-side gather/scatter: HBM, read + write
             ach = 2 * kd["achieved_gbs"]
-            roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                    "traffic": None, "peak_source": hbm_src}
-        else:        # direct mapped-host kernel: bound by the host link (PCIe Gen5 x16)
-            pk = link[kd["peak_key"]] if link else None
-            roof = {"kernel": dom, "bound": "host_link", "achieved": kd["achieved_gbs"], "peak": pk, "unit": "GB/s",
-                    "frac": (kd["achieved_gbs"] / pk) if pk else None, "traffic": None,
-                    "peak_source": "live pinned cudaMemcpyAsync 1 GiB in this run (" +
-                                   ("D2H" if dom == "offload_kernel" else "H2D") + ")"}
+            roof = {"kernel": dom + " (staged device-side piece)", "bound": "hbm", "achieved": ach, "peak": hbm,
+                    "unit": "GB/s", "frac": ach / hbm, "traffic": None, "bytes_per_launch": 2 * kd["bytes_per_launch"],
+                    "ms_per_launch": kd["ms_total"] / kd["launches"], "peak_source": hbm_src}
+        tot_ms = sum(v["ms_total"] for v in kern.values())
+        roof["share_of_transfer_time"] = kd["ms_total"] / tot_ms if tot_ms else None
+    # the step's binding resource is the host link: per-direction DMA/kernel rate and a per-step link roofline
+    link_roof = None
+    if link:
+        bi = link["bidir_gbs"] / 2
+        tmin = 0.0
+        for u, o in step_bytes:
+            lo, hi = min(u, o), max(u, o)
+            uni = link["h2d_gbs"] if u >= o else link["d2h_gbs"]
+            tmin += lo / (bi * 1e9) + (hi - lo) / (uni * 1e9)
+        link_roof = {"bound": "host_link", "step_min_ms": tmin * 1e3 / len(step_bytes),
+                     "step_ms": sum(dev_ms) / len(dev_ms), "frac": tmin * 1e3 / sum(dev_ms),
+                     "how": "per step: min(up,off) at half the measured bidirectional peak + the excess at the "
+                            "unidirectional peak, vs the measured step time"}
+        for k, pk in (("memcpy_d2h", "d2h_gbs"), ("memcpy_h2d", "h2d_gbs"), ("offload_kernel", "d2h_gbs"),
+                      ("upload_kernel", "h2d_gbs")):
+            if k in kern and (k.startswith("memcpy") or roof and roof["bound"] == "host_link"):
+                link_roof[k + "_frac_of_unidir_peak"] = kern[k]["achieved_gbs"] / link[pk]
+                link_roof[k + "_frac_of_bidir_share"] = kern[k]["achieved_gbs"] / bi
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         cpu = cpu_baseline(cfg, args.cpu_seconds)
@@ -324,9 +345,11 @@ def run_ours(args):
         "blocks_per_s": all_blocks / (dev_total_ms * 1e-3),
         "bytes_per_step": all_bytes / n_steps,
         "gpu_launches": int(launches),
+        "memcpy_calls_per_step": (stats["memcpy_calls"] - memcpy0) / n_steps,
         "kernels": kern,
         "hostlink_peak": link,
         "roofline": roof,
+        "roofline_link": link_roof,
         "roofline_device": dev_bench,
         "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": (bytes_up + 16 * all_blocks) / n_steps,
                 "d2h_bytes_per_step": bytes_off / n_steps,

@@ -90,6 +90,7 @@ typedef struct tc_stats_t {
     int64_t kernel_launches, memcpy_calls;     /* cumulative, this pool */
     int64_t bytes_d2h, bytes_h2d;              /* cumulative KV payload bytes enqueued */
     int32_t xfer_d2h, xfer_h2d;                /* effective modes (AUTO resolved) */
+    int64_t reserved_blocks;                   /* claimed by gradual reservations, not yet uploaded into */
 } tc_stats_t;
 
 /* ---- pool lifecycle ------------------------------------------------------------------------------------------ */
@@ -109,6 +110,11 @@ tc_status tc_set_compute_stream(tc_pool *p, void *cuda_stream);
 tc_status tc_streams(tc_pool *p, void **upload_stream, void **offload_stream);
 /* Override the transfer mode per direction (tc_xfer_mode) for subsequent calls. */
 tc_status tc_set_xfer_mode(tc_pool *p, int32_t d2h, int32_t h2d);
+/* Launch configuration of one kernel path: path 0 = direct D2H gather, 1 = direct H2D scatter, 2 = device-side
+   gather/scatter (staged mode and device tier).  ctas <= 0 -> default grid; threads in {32..256} (SIMT variant);
+   variant 0 = SIMT warp-per-chunk 16-byte copies, 1 = TMA bulk copies (cp.async.bulk through a shared-memory ring,
+   one elected thread per CTA).  Results are identical for every setting; only speed differs. */
+tc_status tc_set_launch_config(tc_pool *p, int32_t path, int32_t ctas, int32_t threads, int32_t variant);
 /* Synthetic content: every 8-byte word of the unsharded pool = splitmix64(widx + seed*0xD1B54A32D192ED03), widx its
    index in [L][2][N][T][H][D]; this rank writes its head shard.  Tests/bench only. */
 tc_status tc_fill_kv(tc_pool *p, uint64_t seed);
@@ -142,6 +148,27 @@ tc_status tc_offload_batch(tc_pool *p, int32_t n_agents, const int32_t *agents, 
    tc_handle_info).  Sequential-composition semantics, all-or-nothing.  out_new_ids[offsets[n_handles]]. */
 tc_status tc_upload_batch(tc_pool *p, int32_t n_handles, const tc_handle *hs, const int64_t *offsets,
                           int32_t *out_new_ids);
+/* a8: one whole scheduling cycle in one call — the cycle's uploads (tc_upload_batch arguments) then its offloads
+   (tc_offload_batch arguments).  Everything is validated before anything changes: all-or-nothing, the
+   uploads' status reported first.  Offloads are validated against the pre-cycle state, so they cannot name blocks
+   this cycle's uploads allocate (TC_E_INVAL; reading B5).  The two directions are enqueued interleaved so
+   both host-link directions start as early as possible.  n_handles or n_agents may be 0 (that half is skipped). */
+tc_status tc_cycle(tc_pool *p, int32_t n_handles, const tc_handle *hs, const int64_t *up_offsets,
+                   int32_t *out_new_ids, int32_t n_agents, const int32_t *agents, const int64_t *off_offsets,
+                   const int32_t *block_ids, tc_handle *out_handles);
+
+/* ---- NEXT-1: Gradual GPU Block Reservation ------------------------------------------ */
+/* Plan to claim an offloaded handle's n destination blocks over `cycles` scheduling ticks: chunk t of a near-equal,
+   largest-first split (100/4 -> 25,25,25,25; 10/3 -> 4,3,3).  TC_E_INVAL if cycles < 1 or one is already active. */
+tc_status tc_reserve_begin(tc_pool *p, tc_handle h, int32_t cycles);
+/* One scheduling tick: every handle with an active plan (issue order) claims, under its class's partition rule,
+   up to its cumulative target; a shortfall carries to the next tick.  Claimed blocks are RESERVED: not free,
+   not owned, no data.  tc_upload / tc_upload_batch use them first (claim order), then allocate the remainder. */
+tc_status tc_reserve_tick(tc_pool *p);
+/* Return a handle's reserved blocks to the pool at once (reservation-first return). */
+tc_status tc_reserve_cancel(tc_pool *p, tc_handle h);
+tc_status tc_reserve_info(tc_pool *p, tc_handle h, int64_t *reserved, int64_t *total);   /* readiness */
+
 /* TC_OK if the handle's last transfer has completed, TC_E_BUSY if not, TC_E_HANDLE if unknown. */
 tc_status tc_query(tc_pool *p, tc_handle h);
 tc_status tc_wait(tc_pool *p, tc_handle h);                        /* host-blocking */

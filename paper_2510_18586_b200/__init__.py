@@ -26,8 +26,9 @@ DTYPES = {"fp16": FP16, "bf16": BF16}
 
 SYMBOLS = [
     "tc_pool_desc_init", "tc_pool_create", "tc_pool_create_ex", "tc_pool_destroy", "tc_pool_kv",
-    "tc_set_compute_stream", "tc_streams", "tc_set_xfer_mode", "tc_fill_kv", "tc_partition_reserve",
+    "tc_set_compute_stream", "tc_streams", "tc_set_xfer_mode", "tc_set_launch_config", "tc_fill_kv", "tc_partition_reserve",
     "tc_agent_add", "tc_alloc", "tc_agent_free", "tc_offload", "tc_upload", "tc_offload_batch", "tc_upload_batch",
+    "tc_cycle", "tc_reserve_begin", "tc_reserve_tick", "tc_reserve_cancel", "tc_reserve_info",
     "tc_query", "tc_wait", "tc_stream_wait", "tc_sync", "tc_block_table", "tc_block_table_dev", "tc_handle_info",
     "tc_handle_host", "tc_stats", "tc_timing", "tc_strerror", "tc_last_error", "tc_gather_dev", "tc_scatter_dev",
 ]
@@ -67,6 +68,7 @@ class Stats(ctypes.Structure):
         ("reserved", ctypes.c_int64 * 64), ("claimed", ctypes.c_int64 * 64), ("live_handles", ctypes.c_int64),
         ("kernel_launches", ctypes.c_int64), ("memcpy_calls", ctypes.c_int64), ("bytes_d2h", ctypes.c_int64),
         ("bytes_h2d", ctypes.c_int64), ("xfer_d2h", ctypes.c_int32), ("xfer_h2d", ctypes.c_int32),
+        ("reserved_blocks", ctypes.c_int64),
     ]
 
 
@@ -85,6 +87,7 @@ def _load() -> ctypes.CDLL:
         "tc_set_compute_stream": (I32, [P, VP]),
         "tc_streams": (I32, [P, ctypes.POINTER(VP), ctypes.POINTER(VP)]),
         "tc_set_xfer_mode": (I32, [P, I32, I32]),
+        "tc_set_launch_config": (I32, [P, I32, I32, I32, I32]),
         "tc_fill_kv": (I32, [P, U64]),
         "tc_partition_reserve": (I32, [P, I32, I64]),
         "tc_agent_add": (I32, [P, I32, I32]),
@@ -94,6 +97,11 @@ def _load() -> ctypes.CDLL:
         "tc_upload": (I32, [P, U64, PI32]),
         "tc_offload_batch": (I32, [P, I32, PI32, PI64, PI32, PU64]),
         "tc_upload_batch": (I32, [P, I32, PU64, PI64, PI32]),
+        "tc_cycle": (I32, [P, I32, PU64, PI64, PI32, I32, PI32, PI64, PI32, PU64]),
+        "tc_reserve_begin": (I32, [P, U64, I32]),
+        "tc_reserve_tick": (I32, [P]),
+        "tc_reserve_cancel": (I32, [P, U64]),
+        "tc_reserve_info": (I32, [P, U64, PI64, PI64]),
         "tc_query": (I32, [P, U64]),
         "tc_wait": (I32, [P, U64]),
         "tc_stream_wait": (I32, [P, U64, VP]),
@@ -261,6 +269,50 @@ class Pool:
     def sync(self):
         self._check(lib.tc_sync(self._h))
 
+    def cycle(self, up_handles, off_items):
+        """One scheduling cycle (tc_cycle): uploads of `up_handles`, then offloads [(agent, ids), ...].
+        Returns (new id lists per upload handle, new handles per offload item)."""
+        hs = np.ascontiguousarray(np.asarray(up_handles, dtype=np.uint64).reshape(-1))
+        sizes = []
+        for h in hs:
+            try:
+                sizes.append(self.handle_info(int(h))[1])
+            except TcError:
+                sizes.append(0)
+        uoff = np.zeros(len(hs) + 1, dtype=np.int64)
+        uoff[1:] = np.cumsum(sizes)
+        agents = _i32([a for a, _ in off_items])
+        ooff = np.zeros(len(off_items) + 1, dtype=np.int64)
+        ooff[1:] = np.cumsum([len(x) for _, x in off_items])
+        ids = _i32([b for _, x in off_items for b in x]) if ooff[-1] else np.zeros(1, np.int32)
+        new, out_h = self.cycle_arrays(hs, uoff, agents, ooff, ids)
+        return [new[uoff[k]:uoff[k + 1]].tolist() for k in range(len(hs))], [int(x) for x in out_h]
+
+    def cycle_arrays(self, hs: np.ndarray, uoff: np.ndarray, agents: np.ndarray, ooff: np.ndarray,
+                     ids: np.ndarray):
+        """Zero-copy tc_cycle for prebuilt arrays (bench hot loop)."""
+        new = np.empty(max(int(uoff[-1]), 1), dtype=np.int32)
+        out_h = np.zeros(max(len(agents), 1), dtype=np.uint64)
+        self._check(lib.tc_cycle(self._h, len(hs), _ptr(hs, ctypes.c_uint64), _ptr(uoff, ctypes.c_int64),
+                                 _ptr(new, ctypes.c_int32), len(agents), _ptr(agents, ctypes.c_int32),
+                                 _ptr(ooff, ctypes.c_int64), _ptr(ids, ctypes.c_int32),
+                                 _ptr(out_h, ctypes.c_uint64)))
+        return new[:int(uoff[-1])], out_h[:len(agents)]
+
+    def reserve_begin(self, h: int, cycles: int):
+        self._check(lib.tc_reserve_begin(self._h, h, cycles))
+
+    def reserve_tick(self):
+        self._check(lib.tc_reserve_tick(self._h))
+
+    def reserve_cancel(self, h: int):
+        self._check(lib.tc_reserve_cancel(self._h, h))
+
+    def reserve_info(self, h: int):
+        k, n = ctypes.c_int64(), ctypes.c_int64()
+        self._check(lib.tc_reserve_info(self._h, h, ctypes.byref(k), ctypes.byref(n)))
+        return k.value, n.value
+
     def query(self, h: int) -> bool:
         st = lib.tc_query(self._h, h)
         if st == E_BUSY:
@@ -318,6 +370,10 @@ class Pool:
 
     def set_xfer_mode(self, d2h: int, h2d: int):
         self._check(lib.tc_set_xfer_mode(self._h, d2h, h2d))
+
+    def set_launch_config(self, path: int, ctas: int = 0, threads: int = 256, variant: int = 0):
+        """path 0 = direct D2H, 1 = direct H2D, 2 = device-side (staged/device tier); variant 1 = TMA bulk."""
+        self._check(lib.tc_set_launch_config(self._h, path, ctas, threads, variant))
 
     def fill(self, seed: int):
         self._check(lib.tc_fill_kv(self._h, seed))

@@ -107,6 +107,18 @@ tc_status tc_set_xfer_mode(tc_pool *p, int32_t d2h, int32_t h2d) {
     TC_CATCH
 }
 
+tc_status tc_set_launch_config(tc_pool *p, int32_t path, int32_t ctas, int32_t threads, int32_t variant) {
+    TC_GUARD(p) {
+        if (path < 0 || path > 2 || threads < 32 || threads > 256 || threads % 32 || variant < 0 || variant > 1)
+            return TC_E_INVAL;
+        P.ctas[path] = ctas;
+        P.nthreads[path] = threads;
+        P.variant[path] = variant;
+        return TC_OK;
+    }
+    TC_CATCH
+}
+
 tc_status tc_fill_kv(tc_pool *p, uint64_t seed) {
     TC_GUARD(p) { return P.fill(seed); }
     TC_CATCH
@@ -160,6 +172,42 @@ tc_status tc_offload_batch(tc_pool *p, int32_t n_agents, const int32_t *agents, 
 tc_status tc_upload_batch(tc_pool *p, int32_t n_handles, const tc_handle *hs, const int64_t *offsets,
                           int32_t *out_new_ids) {
     TC_GUARD(p) { return P.upload_batch(n_handles, hs, offsets, out_new_ids); }
+    TC_CATCH
+}
+
+tc_status tc_cycle(tc_pool *p, int32_t n_handles, const tc_handle *hs, const int64_t *up_offsets,
+                   int32_t *out_new_ids, int32_t n_agents, const int32_t *agents, const int64_t *off_offsets,
+                   const int32_t *block_ids, tc_handle *out_handles) {
+    TC_GUARD(p) {
+        return P.cycle(n_handles, hs, up_offsets, out_new_ids, n_agents, agents, off_offsets, block_ids,
+                       out_handles);
+    }
+    TC_CATCH
+}
+
+tc_status tc_reserve_begin(tc_pool *p, tc_handle h, int32_t cycles) {
+    TC_GUARD(p) { return P.reserve_begin(h, cycles); }
+    TC_CATCH
+}
+
+tc_status tc_reserve_tick(tc_pool *p) {
+    TC_GUARD(p) { return P.reserve_tick(); }
+    TC_CATCH
+}
+
+tc_status tc_reserve_cancel(tc_pool *p, tc_handle h) {
+    TC_GUARD(p) { return P.reserve_cancel(h); }
+    TC_CATCH
+}
+
+tc_status tc_reserve_info(tc_pool *p, tc_handle h, int64_t *reserved, int64_t *total) {
+    TC_GUARD(p) {
+        auto it = P.handles.find(h);
+        if (it == P.handles.end()) return TC_E_HANDLE;
+        if (reserved) *reserved = (int64_t)it->second.resv.size();
+        if (total) *total = (int64_t)it->second.pos.size();
+        return TC_OK;
+    }
     TC_CATCH
 }
 
@@ -240,7 +288,8 @@ tc_status tc_stats(tc_pool *p, tc_stats_t *s) {
         int64_t pend = 0;
         for (auto &pc : P.pending_dev) pend += (int64_t)pc.second.size();
         s->pending_blocks = pend;
-        s->alloc_blocks = P.N - P.alloc.nfree - pend;
+        s->alloc_blocks = P.N - P.alloc.nfree - pend - P.n_reserved;
+        s->reserved_blocks = P.n_reserved;
         s->host_slots = P.slots.count;
         s->host_free = (int64_t)P.slots.free_list.size();
         s->host_released = (int64_t)P.slots.released.size();

@@ -16,6 +16,12 @@ struct XferDesc {
 };
 static_assert(sizeof(XferDesc) == 16, "XferDesc must be 16 bytes");
 
+// Staged-mode pieces carry their descriptors by value in the kernel parameters (no host-memory read in the kernel).
+constexpr int kMaxInlineDesc = 128;
+struct InlineDescs {
+    XferDesc d[kMaxInlineDesc];
+};
+
 struct XferGeom {
     int64_t n_pool;      // N
     int64_t chunk;       // C bytes (multiple of 16)
@@ -25,8 +31,13 @@ struct XferGeom {
 // gather: ext[i] + lk*C  <-  kv + (lk*N + blk_i)*C      (a3: offload; epilogue table[tab_i] = -1)
 // scatter: kv + (lk*N + blk_i)*C  <-  ext[i] + lk*C     (a6: upload; epilogue table[tab_i] = blk_i)
 // `desc` may live in mapped pinned memory.  ctas <= 0 selects the default grid.
+// variant 0 = SIMT warp-per-chunk 16-byte copy; 1 = TMA bulk (cp.async.bulk) through a shared-memory ring.
 cudaError_t launch_xfer(bool gather, const XferDesc *desc, int64_t n, const XferGeom &g, void *kv, int32_t *table,
-                        int ctas, int threads, cudaStream_t s);
+                        int ctas, int threads, int variant, cudaStream_t s);
+
+// Same copy as launch_xfer (SIMT variant) with n <= kMaxInlineDesc descriptors passed by value.
+cudaError_t launch_xfer_inline(bool gather, const XferDesc *host_desc, int32_t n, const XferGeom &g, void *kv,
+                               int32_t *table, int ctas, int threads, cudaStream_t s);
 
 // Synthetic content: word w of the unsharded [L][2][N][T][H][D] pool =
 // splitmix64(w + seed * 0xD1B54A32D192ED03); this shard holds heads [rank*Hl, (rank+1)*Hl).

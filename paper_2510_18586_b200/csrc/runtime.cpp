@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <unordered_set>
 
@@ -96,6 +97,8 @@ Pool::~Pool() {
     for (auto e : tev_free) cudaEventDestroy(e);
     if (ev_compute) cudaEventDestroy(ev_compute);
     if (s_up) cudaStreamDestroy(s_up);
+    if (s_up_k) cudaStreamDestroy(s_up_k);
+    if (s_off_k) cudaStreamDestroy(s_off_k);
     if (s_off) cudaStreamDestroy(s_off);
     if (kv_owned && kv) cudaFree(kv);
     if (table_owned && table_dev) cudaFree(table_dev);
@@ -136,10 +139,16 @@ tc_status Pool::create(const tc_pool_desc &d) {
     mode_d2h = d.xfer_d2h;
     mode_h2d = d.xfer_h2d;
     if (mode_d2h < 0 || mode_d2h > 2 || mode_h2d < 0 || mode_h2d > 2) return TC_E_INVAL;
-    ctas_d2h = env_int("TC_CTAS_D2H", 0);
-    ctas_h2d = env_int("TC_CTAS_H2D", 0);
-    ctas_dev = env_int("TC_CTAS_DEV", 0);
-    threads = env_int("TC_THREADS", 256);
+    const char *path_names[3] = {"D2H", "H2D", "DEV"};
+    for (int i = 0; i < 3; ++i) {
+        char nm[32];
+        std::snprintf(nm, sizeof nm, "TC_CTAS_%s", path_names[i]);
+        ctas[i] = env_int(nm, 0);
+        std::snprintf(nm, sizeof nm, "TC_THREADS_%s", path_names[i]);
+        nthreads[i] = env_int(nm, 256);
+        std::snprintf(nm, sizeof nm, "TC_VARIANT_%s", path_names[i]);
+        variant[i] = env_int(nm, 0);
+    }
     if (meta_only) return TC_OK;
 
     TC_CUDA(cudaSetDevice(device), "cudaSetDevice");
@@ -147,6 +156,10 @@ tc_status Pool::create(const tc_pool_desc &d) {
     TC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
     TC_CUDA(cudaStreamCreateWithPriority(&s_up, cudaStreamNonBlocking, hi), "upload stream");   // P:646 first
     TC_CUDA(cudaStreamCreateWithPriority(&s_off, cudaStreamNonBlocking, lo), "offload stream");
+    TC_CUDA(cudaStreamCreateWithPriority(&s_up_k, cudaStreamNonBlocking, hi), "upload aux stream");
+    TC_CUDA(cudaStreamCreateWithPriority(&s_off_k, cudaStreamNonBlocking, lo), "offload aux stream");
+    piece_bytes = env_int("TC_PIECE_KIB", 32768) * 1024ll;
+    use_batch_memcpy = env_int("TC_BATCH_MEMCPY", 1) != 0;
     TC_CUDA(cudaEventCreateWithFlags(&ev_compute, cudaEventDisableTiming), "event");
     const int64_t kv_bytes = (int64_t)L * 2 * N * C;
     if (d.kv_dev) {
@@ -178,8 +191,10 @@ tc_status Pool::create(const tc_pool_desc &d) {
     TC_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&ring_dev), ring_host, 0), "ring dev ptr");
     staging_bytes = d.staging_bytes > 0 ? d.staging_bytes : (256ll << 20);
     if (staging_bytes < B) staging_bytes = B;
-    if (mode_d2h == TC_XFER_AUTO) mode_d2h = env_int("TC_AUTO_D2H", TC_XFER_DIRECT);
-    if (mode_h2d == TC_XFER_AUTO) mode_h2d = env_int("TC_AUTO_H2D", TC_XFER_DIRECT);
+    // AUTO: the copy-engine staged path measured faster than the SM direct path in both directions on B200
+    // (profiles/r01_xfer_probe.json: alone 57.1 vs 52.6 GB/s D2H, 55.4 vs 51.3 H2D; concurrent 53.7+49.7 vs 45+40).
+    if (mode_d2h == TC_XFER_AUTO) mode_d2h = env_int("TC_AUTO_D2H", TC_XFER_STAGED);
+    if (mode_h2d == TC_XFER_AUTO) mode_h2d = env_int("TC_AUTO_H2D", TC_XFER_STAGED);
     for (int i = 0; i < 16; ++i) {
         cudaEvent_t e;
         TC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -273,92 +288,183 @@ char *Pool::ring_alloc(int64_t bytes, char **dev_ptr) {
     return h;
 }
 
-// Enqueue one transfer of desc.size() blocks on stream s.  gather = offload direction (pool -> ext).
-// slot_of[i] = host slot of block i (or -1 for the device tier, where desc[i].ext is already set).
-tc_status Pool::enqueue_xfer(bool gather, int32_t mode, const std::vector<XferDesc> &desc_in,
-                             const std::vector<int64_t> &slot_of, cudaStream_t s) {
-    const int64_t n = (int64_t)desc_in.size();
+// A transfer of desc.size() blocks, enqueued in two phases so that one scheduling cycle can interleave its two
+// directions on the host (tc_cycle) and both links start as early as possible:
+//   DIRECT          A = the single kernel over mapped host memory                 B = -
+//   STAGED gather   A = every piece's gather kernel (aux stream) + an event each  B = the D2H copy per piece (main)
+//   STAGED scatter  A = the H2D copy per piece (main) + an event each             B = the scatter per piece (aux)
+// Pieces of <= pb blocks pipeline the device-side kernels against the copy engine.  If the batch needs more pieces
+// than the staging ring holds (R), phase A does the whole transfer piece by piece (ring reuse waits), B nothing.
+tc_status Pool::xfer_init(XferJob &j, bool gather, int32_t mode, const std::vector<XferDesc> *desc,
+                          const std::vector<int64_t> *slot_of, cudaStream_t s) {
+    j.gather = gather;
+    j.mode = (slot_of == nullptr || slot_of->empty()) ? TC_XFER_DIRECT : mode;
+    j.desc = desc;
+    j.slot_of = slot_of;
+    j.s = s;
+    j.n = (int64_t)desc->size();
+    if (j.mode != TC_XFER_STAGED || j.n == 0) return TC_OK;
+    const int dir = gather ? 0 : 1;
+    if (!staging[dir]) TC_CUDA(cudaMalloc(&staging[dir], staging_bytes), "staging alloc");
+    j.stg = staging[dir];
+    j.sk = gather ? s_off_k : s_up_k;
+    j.pb = std::max<int64_t>(1, std::min<int64_t>({(int64_t)kMaxInlineDesc, piece_bytes / B, staging_bytes / B}));
+    j.R = std::max<int64_t>(1, staging_bytes / (j.pb * B));
+    j.npieces = (j.n + j.pb - 1) / j.pb;
+    j.ring_reuse = j.npieces > j.R;
+    j.ev.assign(j.npieces, -1);
+    int32_t e0;
+    tc_status st = ev_rec(s, &e0);                  // the aux stream starts after the main stream's waits
+    if (st != TC_OK) return st;
+    TC_CUDA(cudaStreamWaitEvent(j.sk, events[e0], 0), "aux wait");
+    return TC_OK;
+}
+
+tc_status Pool::ev_rec(cudaStream_t st, int32_t *out) {
+    *out = event_get();
+    if (*out < 0) return cuda_fail(cudaErrorMemoryAllocation, "event pool");
+    TC_CUDA(cudaEventRecord(events[*out], st), "piece event");
+    return TC_OK;
+}
+
+// Copy-engine DMA of pieces [a, b) between the staging slot `base` and the host slots (one call per piece).
+tc_status Pool::xfer_copy(XferJob &j, int64_t a, int64_t b, char *base) {
+    const bool to_host = j.gather;
+    const auto &slot_of = *j.slot_of;
+    cudaEvent_t t0;
+    tc_status s0 = span_begin(j.s, &t0);
+    if (s0 != TC_OK) return s0;
+    cp_dst.clear(); cp_src.clear(); cp_size.clear();
+    for (int64_t i = a; i < b;) {
+        int64_t k = i + 1;
+        while (k < b && slot_of[k] == slot_of[k - 1] + 1) ++k;      // contiguous run of host slots
+        char *hp = slots.host + slot_of[i] * B;
+        char *dp = base + (i - a) * B;
+        cp_dst.push_back(to_host ? (void *)hp : (void *)dp);
+        cp_src.push_back(to_host ? (void *)dp : (void *)hp);
+        cp_size.push_back((size_t)((k - i) * B));
+        i = k;
+    }
+    if (cp_dst.size() > 1 && use_batch_memcpy) {
+        cudaMemcpyAttributes attr{};
+        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+        attr.flags = cudaMemcpyFlagDefault;
+        size_t attr_idx = 0, fail_idx = 0;
+        cudaError_t e = cudaMemcpyBatchAsync(cp_dst.data(), cp_src.data(), cp_size.data(), cp_dst.size(), &attr,
+                                             &attr_idx, 1, &fail_idx, j.s);
+        if (e == cudaSuccess) {
+            ++n_memcpy;
+            return span_end(j.s, to_host ? 3 : 4, t0, (b - a) * B);
+        }
+        cudaGetLastError();          // not supported here: fall back to one call per run, permanently
+        use_batch_memcpy = false;
+    }
+    for (size_t r = 0; r < cp_dst.size(); ++r) {
+        TC_CUDA(cudaMemcpyAsync(cp_dst[r], cp_src[r], cp_size[r],
+                                to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, j.s),
+                "staged memcpy");
+        ++n_memcpy;
+    }
+    return span_end(j.s, to_host ? 3 : 4, t0, (b - a) * B);
+}
+
+// Device-side gather/scatter of pieces [a, b) against the staging slot `base`, descriptors by value.
+tc_status Pool::xfer_kernel(XferJob &j, int64_t a, int64_t b, char *base) {
+    XferDesc pd[kMaxInlineDesc];
+    for (int64_t i = a; i < b; ++i) {
+        pd[i - a] = (*j.desc)[i];
+        pd[i - a].ext = reinterpret_cast<uint64_t>(base + (i - a) * B);
+    }
     const XferGeom g{N, C, 2 * L};
-    const int ctas = slot_of.empty() ? ctas_dev : (gather ? ctas_d2h : ctas_h2d);
-    if (slot_of.empty() || mode == TC_XFER_DIRECT) {
+    cudaEvent_t t0;
+    tc_status s0 = span_begin(j.sk, &t0);
+    if (s0 != TC_OK) return s0;
+    TC_CUDA(launch_xfer_inline(j.gather, pd, (int32_t)(b - a), g, kv, table_dev, ctas[2], nthreads[2], j.sk),
+            j.gather ? "gather kernel" : "scatter kernel");
+    ++n_launch;
+    return span_end(j.sk, j.gather ? 0 : 1, t0, (b - a) * B);
+}
+
+tc_status Pool::xfer_phase_a(XferJob &j) {
+    if (j.n == 0) return TC_OK;
+    const XferGeom g{N, C, 2 * L};
+    tc_status st;
+    if (j.mode == TC_XFER_DIRECT) {
+        const bool dev_tier = j.slot_of == nullptr || j.slot_of->empty();
+        const int path = dev_tier ? 2 : (j.gather ? 0 : 1);
         char *dptr = nullptr;
-        char *h = ring_alloc(n * (int64_t)sizeof(XferDesc), &dptr);
+        char *h = ring_alloc(j.n * (int64_t)sizeof(XferDesc), &dptr);
         if (!h) return cuda_fail(cudaErrorMemoryAllocation, "descriptor ring");
         XferDesc *hd = reinterpret_cast<XferDesc *>(h);
-        for (int64_t i = 0; i < n; ++i) {
-            hd[i] = desc_in[i];
-            if (!slot_of.empty()) hd[i].ext = reinterpret_cast<uint64_t>(slots.dev + slot_of[i] * B);
+        for (int64_t i = 0; i < j.n; ++i) {
+            hd[i] = (*j.desc)[i];
+            if (!dev_tier) hd[i].ext = reinterpret_cast<uint64_t>(slots.dev + (*j.slot_of)[i] * B);
         }
         cudaEvent_t t0;
-        tc_status st = span_begin(s, &t0);
-        if (st != TC_OK) return st;
-        TC_CUDA(launch_xfer(gather, reinterpret_cast<const XferDesc *>(dptr), n, g, kv, table_dev, ctas, threads, s),
+        if ((st = span_begin(j.s, &t0)) != TC_OK) return st;
+        TC_CUDA(launch_xfer(j.gather, reinterpret_cast<const XferDesc *>(dptr), j.n, g, kv, table_dev, ctas[path],
+                            nthreads[path], variant[path], j.s),
                 "xfer kernel");
         ++n_launch;
-        return span_end(s, slot_of.empty() ? 2 : (gather ? 0 : 1), t0, n * B);
+        return span_end(j.s, path == 2 ? 2 : (j.gather ? 0 : 1), t0, j.n * B);
     }
-    // STAGED: device staging ring + copy-engine DMA over contiguous runs of host slots, in ring-sized pieces.
-    char *stg = staging[gather ? 0 : 1];
-    if (!stg) {
-        TC_CUDA(cudaMalloc(&staging[gather ? 0 : 1], staging_bytes), "staging alloc");
-        stg = staging[gather ? 0 : 1];
-    }
-    const int64_t per = std::max<int64_t>(1, staging_bytes / B);
-    for (int64_t a = 0; a < n; a += per) {
-        const int64_t b = std::min(n, a + per);
-        char *dptr = nullptr;
-        char *h = ring_alloc((b - a) * (int64_t)sizeof(XferDesc), &dptr);
-        if (!h) return cuda_fail(cudaErrorMemoryAllocation, "descriptor ring");
-        XferDesc *hd = reinterpret_cast<XferDesc *>(h);
-        for (int64_t i = a; i < b; ++i) {
-            hd[i - a] = desc_in[i];
-            hd[i - a].ext = reinterpret_cast<uint64_t>(stg + (i - a) * B);
-        }
-        auto copy_runs = [&](bool to_host) -> tc_status {
-            cudaEvent_t t0;
-            tc_status st0 = span_begin(s, &t0);
-            if (st0 != TC_OK) return st0;
-            int64_t i = a;
-            while (i < b) {
-                int64_t j = i + 1;
-                while (j < b && slot_of[j] == slot_of[j - 1] + 1) ++j;
-                char *hp = slots.host + slot_of[i] * B;
-                char *dp = stg + (i - a) * B;
-                TC_CUDA(cudaMemcpyAsync(to_host ? (void *)hp : (void *)dp, to_host ? (void *)dp : (void *)hp,
-                                        (size_t)((j - i) * B), to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice,
-                                        s),
-                        "staged memcpy");
-                ++n_memcpy;
-                i = j;
+    std::vector<int32_t> done(j.ring_reuse ? j.npieces : 0, -1);
+    for (int64_t p = 0; p < j.npieces; ++p) {
+        const int64_t a = p * j.pb, b = std::min(j.n, a + j.pb);
+        char *base = j.stg + (p % j.R) * j.pb * B;
+        if (j.gather) {
+            if (j.ring_reuse && p >= j.R) TC_CUDA(cudaStreamWaitEvent(j.sk, events[done[p - j.R]], 0), "ring reuse");
+            if ((st = xfer_kernel(j, a, b, base)) != TC_OK) return st;
+            if ((st = ev_rec(j.sk, &j.ev[p])) != TC_OK) return st;
+            if (j.ring_reuse) {                        // interleaved: copy now, mark the ring slot free after it
+                TC_CUDA(cudaStreamWaitEvent(j.s, events[j.ev[p]], 0), "gather->D2H wait");
+                if ((st = xfer_copy(j, a, b, base)) != TC_OK) return st;
+                if ((st = ev_rec(j.s, &done[p])) != TC_OK) return st;
             }
-            return span_end(s, to_host ? 3 : 4, t0, (b - a) * B);
-        };
-        cudaEvent_t t0;
-        if (gather) {
-            tc_status st = span_begin(s, &t0);
-            if (st != TC_OK) return st;
-            TC_CUDA(launch_xfer(true, reinterpret_cast<const XferDesc *>(dptr), b - a, g, kv, table_dev, ctas_dev,
-                                threads, s),
-                    "gather kernel");
-            ++n_launch;
-            st = span_end(s, 0, t0, (b - a) * B);
-            if (st != TC_OK) return st;
-            st = copy_runs(true);
-            if (st != TC_OK) return st;
         } else {
-            tc_status st = copy_runs(false);
-            if (st != TC_OK) return st;
-            st = span_begin(s, &t0);
-            if (st != TC_OK) return st;
-            TC_CUDA(launch_xfer(false, reinterpret_cast<const XferDesc *>(dptr), b - a, g, kv, table_dev, ctas_dev,
-                                threads, s),
-                    "scatter kernel");
-            ++n_launch;
-            st = span_end(s, 1, t0, (b - a) * B);
-            if (st != TC_OK) return st;
+            if (j.ring_reuse && p >= j.R) TC_CUDA(cudaStreamWaitEvent(j.s, events[done[p - j.R]], 0), "ring reuse");
+            if ((st = xfer_copy(j, a, b, base)) != TC_OK) return st;
+            if ((st = ev_rec(j.s, &j.ev[p])) != TC_OK) return st;
+            if (j.ring_reuse) {
+                TC_CUDA(cudaStreamWaitEvent(j.sk, events[j.ev[p]], 0), "H2D->scatter wait");
+                if ((st = xfer_kernel(j, a, b, base)) != TC_OK) return st;
+                if ((st = ev_rec(j.sk, &done[p])) != TC_OK) return st;
+            }
         }
+    }
+    if (j.ring_reuse && !j.gather) TC_CUDA(cudaStreamWaitEvent(j.s, events[done[j.npieces - 1]], 0), "join");
+    return TC_OK;
+}
+
+tc_status Pool::xfer_phase_b(XferJob &j) {
+    if (j.n == 0 || j.mode != TC_XFER_STAGED || j.ring_reuse) return TC_OK;
+    tc_status st;
+    int32_t last = -1;
+    for (int64_t p = 0; p < j.npieces; ++p) {
+        const int64_t a = p * j.pb, b = std::min(j.n, a + j.pb);
+        char *base = j.stg + (p % j.R) * j.pb * B;
+        if (j.gather) {
+            TC_CUDA(cudaStreamWaitEvent(j.s, events[j.ev[p]], 0), "gather->D2H wait");
+            if ((st = xfer_copy(j, a, b, base)) != TC_OK) return st;
+        } else {
+            TC_CUDA(cudaStreamWaitEvent(j.sk, events[j.ev[p]], 0), "H2D->scatter wait");
+            if ((st = xfer_kernel(j, a, b, base)) != TC_OK) return st;
+        }
+    }
+    if (!j.gather) {                                   // the upload completes when its last scatter has
+        if ((st = ev_rec(j.sk, &last)) != TC_OK) return st;
+        TC_CUDA(cudaStreamWaitEvent(j.s, events[last], 0), "scatter->upload join");
     }
     return TC_OK;
+}
+
+tc_status Pool::enqueue_xfer(bool gather, int32_t mode, const std::vector<XferDesc> &desc,
+                             const std::vector<int64_t> &slot_of, cudaStream_t s) {
+    XferJob j;
+    tc_status st = xfer_init(j, gather, mode, &desc, &slot_of, s);
+    if (st == TC_OK) st = xfer_phase_a(j);
+    if (st == TC_OK) st = xfer_phase_b(j);
+    return st;
 }
 
 // Device block-table rows follow host-side appends (decode growth) on the stream the agent's compute reads from.
@@ -433,12 +539,10 @@ tc_status Pool::agent_free(int32_t a) {
     return TC_OK;
 }
 
-tc_status Pool::offload_batch(int32_t na, const int32_t *ags, const int64_t *off, const int32_t *ids,
-                              tc_handle *out) {
-    if (cuda_dead) return TC_E_CUDA;
-    if (na < 1 || !ags || !off || !ids || !out || off[0] != 0) return TC_E_INVAL;
-    // a2 admission: validate everything before touching state (A5, A15), item by item in order so that the first
-    // failing item decides the status (sequential-composition semantics of a batch)
+// a2 admission: validate everything before touching state (A5, A15), item by item in order so that the first failing
+// item decides the status (sequential-composition semantics of a batch, reading B1).
+tc_status Pool::plan_offload(OffPlan &P, int32_t na, const int32_t *ags, const int64_t *off, const int32_t *ids) {
+    if (na < 1 || !ags || !off || !ids || off[0] != 0) return TC_E_INVAL;
     if (++epoch == 0) { std::fill(stamp.begin(), stamp.end(), 0); epoch = 1; }
     for (int32_t k = 0; k < na; ++k) {
         const int32_t a = ags[k];
@@ -450,39 +554,40 @@ tc_status Pool::offload_batch(int32_t na, const int32_t *ags, const int64_t *off
                 return TC_E_INVAL;
             stamp[b] = epoch;
         }
-        if ((int64_t)slots.free_list.size() < off[k + 1]) return TC_E_NOHOST;   // refuse
+        if ((int64_t)slots.free_list.size() < off[k + 1]) return TC_E_NOHOST;   // refuse, no change
     }
+    P.na = na; P.ags = ags; P.off = off; P.ids = ids;
     const int64_t n = off[na];
-
-    std::vector<XferDesc> desc(n);
-    std::vector<int64_t> slot_of(n);
+    P.desc.resize(n);
+    P.slot_of.resize(n);
     const size_t top = slots.free_list.size();
-    for (int64_t i = 0; i < n; ++i) slot_of[i] = slots.free_list[top - 1 - i];   // LIFO pop order
+    for (int64_t i = 0; i < n; ++i) P.slot_of[i] = slots.free_list[top - 1 - i];   // LIFO pop order (A16)
     for (int32_t k = 0; k < na; ++k)
         for (int64_t i = off[k]; i < off[k + 1]; ++i)
-            desc[i] = XferDesc{ids[i], ags[k] * max_bpa + alloc.own_pos[ids[i]], 0};
+            P.desc[i] = XferDesc{ids[i], ags[k] * max_bpa + alloc.own_pos[ids[i]], 0};
+    return TC_OK;
+}
 
-    int32_t ev = -1;
-    if (!meta_only) {
-        if (s_compute) {   // capture the agents' last decode writes (GPU-side, no host block)
-            TC_CUDA(cudaEventRecord(ev_compute, s_compute), "compute event");
-            TC_CUDA(cudaStreamWaitEvent(s_off, ev_compute, 0), "compute wait");
-        }
-        for (int32_t k = 0; k < na; ++k) {   // blocks still being written by an upload of this agent
-            const int32_t ue = agents[ags[k]].up_event;
-            if (ue >= 0) TC_CUDA(cudaStreamWaitEvent(s_off, events[ue], 0), "upload->offload wait");
-        }
-        tc_status st = enqueue_xfer(true, mode_d2h, desc, slot_of, s_off);
-        if (st != TC_OK) return st;
-        ev = event_get();
-        if (ev < 0) return cuda_fail(cudaErrorMemoryAllocation, "event pool");
-        TC_CUDA(cudaEventRecord(events[ev], s_off), "offload event");
-        bytes_d2h += n * B;
+// GPU-side dependencies of an offload: the compute stream (the agents' last decode writes) and any upload into
+// these agents since the last sync.
+tc_status Pool::offload_waits(const OffPlan &P) {
+    if (s_compute) {
+        TC_CUDA(cudaEventRecord(ev_compute, s_compute), "compute event");
+        TC_CUDA(cudaStreamWaitEvent(s_off, ev_compute, 0), "compute wait");
     }
-    // commit (a3 logical effects + a4 pending free)
-    slots.free_list.resize(top - n);
-    for (int32_t k = 0; k < na; ++k) {
-        const int32_t a = ags[k];
+    for (int32_t k = 0; k < P.na; ++k) {
+        const int32_t ue = agents[P.ags[k]].up_event;
+        if (ue >= 0) TC_CUDA(cudaStreamWaitEvent(s_off, events[ue], 0), "upload->offload wait");
+    }
+    return TC_OK;
+}
+
+// commit (a3 logical effects + a4 pending free); ev = the offload's completion event
+void Pool::commit_offload(const OffPlan &P, int32_t ev, tc_handle *out) {
+    const int64_t n = P.off[P.na];
+    slots.free_list.resize(slots.free_list.size() - n);
+    for (int32_t k = 0; k < P.na; ++k) {
+        const int32_t a = P.ags[k];
         AgentRec &ag = agents[a];
         HandleRec hr;
         hr.agent = a;
@@ -490,13 +595,13 @@ tc_status Pool::offload_batch(int32_t na, const int32_t *ags, const int64_t *off
         hr.state = kOffloaded;
         hr.ev = ev;
         std::vector<int32_t> pend;
-        for (int64_t i = off[k]; i < off[k + 1]; ++i) {
-            const int32_t b = ids[i];
+        for (int64_t i = P.off[k]; i < P.off[k + 1]; ++i) {
+            const int32_t b = P.ids[i];
             const int32_t p = alloc.own_pos[b];
             hr.pos.push_back(p);
-            hr.slots.push_back(slot_of[i]);
-            ag.table[p] = -1;
-            alloc.state[b] = kPending;
+            hr.slots.push_back(P.slot_of[i]);
+            ag.table[p] = -1;                              // location flag -> host
+            alloc.state[b] = kPending;                     // pending free until tc_sync
             alloc.own_agent[b] = -1;
             alloc.own_pos[b] = -1;
             pend.push_back(b);
@@ -507,81 +612,227 @@ tc_status Pool::offload_batch(int32_t na, const int32_t *ags, const int64_t *off
         handles.emplace(h, std::move(hr));
         out[k] = h;
     }
-    return TC_OK;
+    if (!meta_only) bytes_d2h += n * B;
 }
 
-tc_status Pool::upload_batch(int32_t nh, const tc_handle *hs, const int64_t *off, int32_t *out_ids) {
-    if (cuda_dead) return TC_E_CUDA;
-    if (nh < 1 || !hs || !off || !out_ids || off[0] != 0) return TC_E_INVAL;
-    std::vector<HandleRec *> hr(nh);
-    // validate + a5 dry run on counters only, item by item in order (first failing item decides the status)
+// validate + a5 dry run on counters only, item by item in order.  Blocks already claimed by a gradual reservation
+// are used first (claim order); only the remainder is allocated, lowest free first.
+tc_status Pool::plan_upload(UpPlan &P, int32_t nh, const tc_handle *hs, const int64_t *off) {
+    if (nh < 1 || !hs || !off || off[0] != 0) return TC_E_INVAL;
+    P.hr.assign(nh, nullptr);
+    P.rr.assign(nh, 0);
+    P.need.assign(nh, 0);
     std::vector<int64_t> cl = alloc.claimed;
-    std::vector<int64_t> rr(nh);
     int64_t nf = alloc.nfree;
     std::unordered_set<tc_handle> seen;
     for (int32_t k = 0; k < nh; ++k) {
         auto it = handles.find(hs[k]);
         if (it == handles.end() || it->second.state != kOffloaded || !seen.insert(hs[k]).second) return TC_E_HANDLE;
-        hr[k] = &it->second;
+        P.hr[k] = &it->second;
         const int64_t k_n = off[k + 1] - off[k];
-        if (k_n != (int64_t)hr[k]->pos.size()) return TC_E_INVAL;
-        const int64_t r = BlockAllocator::plan(hr[k]->cls, k_n, nf, alloc.reserved, cl);
+        if (k_n != (int64_t)P.hr[k]->pos.size()) return TC_E_INVAL;
+        P.need[k] = k_n - (int64_t)P.hr[k]->resv.size();
+        const int64_t r = P.need[k] > 0 ? BlockAllocator::plan(P.hr[k]->cls, P.need[k], nf, alloc.reserved, cl) : 0;
         if (r < 0) return TC_E_NOBLOCKS;      // upload "stalls"; handles stay valid
-        rr[k] = r;
-        cl[hr[k]->cls] += r;
-        nf -= k_n;
+        P.rr[k] = r;
+        cl[P.hr[k]->cls] += r;
+        nf -= std::max<int64_t>(0, P.need[k]);
     }
+    P.nh = nh; P.hs = hs; P.off = off;
     const int64_t n = off[nh];
-    // sequential composition of lowest-free-first == the n lowest free ids split in order
-    std::vector<int32_t> fresh(n);
+    P.n_fresh = 0;
+    for (int32_t k = 0; k < nh; ++k) P.n_fresh += P.need[k];
+    // sequential composition of lowest-free-first == the n_fresh lowest free ids split in order
+    std::vector<int32_t> fresh(P.n_fresh);
     {
         int64_t got = 0;
-        for (int64_t w = alloc.hint; got < n && w < (int64_t)alloc.bits.size(); ++w)
-            for (uint64_t x = alloc.bits[w]; x && got < n; x &= x - 1) fresh[got++] = (int32_t)(w * 64 + __builtin_ctzll(x));
+        for (int64_t w = alloc.hint; got < P.n_fresh && w < (int64_t)alloc.bits.size(); ++w)
+            for (uint64_t x = alloc.bits[w]; x && got < P.n_fresh; x &= x - 1)
+                fresh[got++] = (int32_t)(w * 64 + __builtin_ctzll(x));
     }
-    std::vector<XferDesc> desc(n);
-    std::vector<int64_t> slot_of(n);
-    for (int32_t k = 0; k < nh; ++k)
-        for (int64_t i = off[k]; i < off[k + 1]; ++i) {
-            const int64_t q = i - off[k];
-            desc[i] = XferDesc{fresh[i], hr[k]->agent * max_bpa + hr[k]->pos[q], 0};
-            slot_of[i] = hr[k]->slots[q];
-        }
-    int32_t ev = -1;
-    if (!meta_only) {
-        for (int32_t k = 0; k < nh; ++k)      // A13: the upload waits for the handle's offload (GPU-side)
-            if (hr[k]->ev >= 0) TC_CUDA(cudaStreamWaitEvent(s_up, events[hr[k]->ev], 0), "offload->upload wait");
-        tc_status st = enqueue_xfer(false, mode_h2d, desc, slot_of, s_up);
-        if (st != TC_OK) return st;
-        ev = event_get();
-        if (ev < 0) return cuda_fail(cudaErrorMemoryAllocation, "event pool");
-        TC_CUDA(cudaEventRecord(events[ev], s_up), "upload event");
-        bytes_h2d += n * B;
-    }
-    // commit (a5 allocation, a6 remap, a7 released slots)
-    {
-        std::vector<int32_t> taken(n);
-        alloc.take_lowest(n, taken.data());   // identical to `fresh` (same scan, nothing changed in between)
-    }
+    P.dst.resize(n);
+    P.desc.resize(n);
+    P.slot_of.resize(n);
+    int64_t f = 0;
     for (int32_t k = 0; k < nh; ++k) {
-        HandleRec &h = *hr[k];
-        AgentRec &ag = agents[h.agent];
-        alloc.claimed[h.cls] += rr[k];
-        for (int64_t i = off[k]; i < off[k + 1]; ++i) {
+        int64_t i = off[k];
+        for (int32_t b : P.hr[k]->resv) P.dst[i++] = b;
+        for (; i < off[k + 1]; ++i) P.dst[i] = fresh[f++];
+        for (i = off[k]; i < off[k + 1]; ++i) {
             const int64_t q = i - off[k];
-            const int32_t b = fresh[i];
+            P.desc[i] = XferDesc{P.dst[i], P.hr[k]->agent * max_bpa + P.hr[k]->pos[q], 0};
+            P.slot_of[i] = P.hr[k]->slots[q];
+        }
+    }
+    return TC_OK;
+}
+
+tc_status Pool::upload_waits(const UpPlan &P) {          // A13: the upload waits for each handle's offload
+    for (int32_t k = 0; k < P.nh; ++k)
+        if (P.hr[k]->ev >= 0) TC_CUDA(cudaStreamWaitEvent(s_up, events[P.hr[k]->ev], 0), "offload->upload wait");
+    return TC_OK;
+}
+
+// commit (a5 allocation, a6 remap, a7 released slots); ev = the upload's completion event
+void Pool::commit_upload(const UpPlan &P, int32_t ev, int32_t *out_ids) {
+    if (P.n_fresh > 0) {
+        std::vector<int32_t> taken(P.n_fresh);
+        alloc.take_lowest(P.n_fresh, taken.data());   // identical to the planned ids (nothing changed since)
+    }
+    for (int32_t k = 0; k < P.nh; ++k) {
+        HandleRec &h = *P.hr[k];
+        AgentRec &ag = agents[h.agent];
+        alloc.claimed[h.cls] += P.rr[k];
+        n_reserved -= (int64_t)h.resv.size();
+        for (int64_t i = P.off[k]; i < P.off[k + 1]; ++i) {
+            const int64_t q = i - P.off[k];
+            const int32_t b = P.dst[i];
             alloc.state[b] = kAlloc;
             alloc.own_agent[b] = h.agent;
             alloc.own_pos[b] = h.pos[q];
-            ag.table[h.pos[q]] = b;
+            ag.table[h.pos[q]] = b;                        // fused remap's host mirror (A6)
             slots.released.push_back(h.slots[q]);
             out_ids[i] = b;
         }
+        h.resv.clear();
+        h.plan.clear();
+        resv_active.erase(P.hs[k]);
         h.state = kUploaded;
         h.ev = ev;
         --ag.live_offloads;
         ag.up_event = ev;
     }
+    if (!meta_only) bytes_h2d += P.off[P.nh] * B;
+}
+
+tc_status Pool::offload_batch(int32_t na, const int32_t *ags, const int64_t *off, const int32_t *ids,
+                              tc_handle *out) {
+    if (cuda_dead) return TC_E_CUDA;
+    if (!out) return TC_E_INVAL;
+    OffPlan P;
+    tc_status st = plan_offload(P, na, ags, off, ids);
+    if (st != TC_OK) return st;
+    int32_t ev = -1;
+    if (!meta_only) {
+        if ((st = offload_waits(P)) != TC_OK) return st;
+        if ((st = enqueue_xfer(true, mode_d2h, P.desc, P.slot_of, s_off)) != TC_OK) return st;
+        if ((st = ev_rec(s_off, &ev)) != TC_OK) return st;
+    }
+    commit_offload(P, ev, out);
+    return TC_OK;
+}
+
+tc_status Pool::upload_batch(int32_t nh, const tc_handle *hs, const int64_t *off, int32_t *out_ids) {
+    if (cuda_dead) return TC_E_CUDA;
+    if (!out_ids) return TC_E_INVAL;
+    UpPlan P;
+    tc_status st = plan_upload(P, nh, hs, off);
+    if (st != TC_OK) return st;
+    int32_t ev = -1;
+    if (!meta_only) {
+        if ((st = upload_waits(P)) != TC_OK) return st;
+        if ((st = enqueue_xfer(false, mode_h2d, P.desc, P.slot_of, s_up)) != TC_OK) return st;
+        if ((st = ev_rec(s_up, &ev)) != TC_OK) return st;
+    }
+    commit_upload(P, ev, out_ids);
+    return TC_OK;
+}
+
+// a8: one scheduling cycle = this cycle's uploads, then its offloads, as one call.  Both are validated
+// before anything changes (all-or-nothing; uploads' status first).  The offloads are validated against the pre-cycle
+// state, so they cannot name blocks this cycle's uploads allocate (reading B5).  The two directions are enqueued
+// interleaved — H2D copies, gathers, D2H copies, scatters — so both links start as early as possible.
+tc_status Pool::cycle(int32_t nh, const tc_handle *hs, const int64_t *up_off, int32_t *out_ids, int32_t na,
+                      const int32_t *ags, const int64_t *off_off, const int32_t *ids, tc_handle *out_h) {
+    if (cuda_dead) return TC_E_CUDA;
+    if (nh < 0 || na < 0 || (nh > 0 && !out_ids) || (na > 0 && !out_h)) return TC_E_INVAL;
+    UpPlan U;
+    OffPlan O;
+    tc_status st;
+    if (nh > 0 && (st = plan_upload(U, nh, hs, up_off)) != TC_OK) return st;
+    if (na > 0 && (st = plan_offload(O, na, ags, off_off, ids)) != TC_OK) return st;
+    int32_t ev_up = -1, ev_off = -1;
+    if (!meta_only) {
+        XferJob ju, jo;
+        if (nh > 0) {
+            if ((st = upload_waits(U)) != TC_OK) return st;
+            if ((st = xfer_init(ju, false, mode_h2d, &U.desc, &U.slot_of, s_up)) != TC_OK) return st;
+            if ((st = xfer_phase_a(ju)) != TC_OK) return st;          // H2D copies start first
+        }
+        if (na > 0) {
+            if ((st = offload_waits(O)) != TC_OK) return st;
+            if ((st = xfer_init(jo, true, mode_d2h, &O.desc, &O.slot_of, s_off)) != TC_OK) return st;
+            if ((st = xfer_phase_a(jo)) != TC_OK) return st;          // gathers
+            if ((st = xfer_phase_b(jo)) != TC_OK) return st;          // D2H copies
+            if ((st = ev_rec(s_off, &ev_off)) != TC_OK) return st;
+        }
+        if (nh > 0) {
+            if ((st = xfer_phase_b(ju)) != TC_OK) return st;          // scatters + remap
+            if ((st = ev_rec(s_up, &ev_up)) != TC_OK) return st;
+        }
+    }
+    if (nh > 0) commit_upload(U, ev_up, out_ids);
+    if (na > 0) commit_offload(O, ev_off, out_h);
+    return TC_OK;
+}
+
+// ------------------------------------------------------------------------------------------------ NEXT-1
+// Gradual GPU Block Reservation: claim an offloaded handle's destination blocks over several
+// scheduling ticks so the predictive upload never stalls on allocation.  Chunks are near-equal, largest first;
+// each tick claims up to the cumulative target, a shortfall carries to the next tick.
+tc_status Pool::reserve_begin(tc_handle h, int32_t cycles) {
+    auto it = handles.find(h);
+    if (it == handles.end() || it->second.state != kOffloaded) return TC_E_HANDLE;
+    HandleRec &hd = it->second;
+    if (cycles < 1 || !hd.plan.empty() || !hd.resv.empty()) return TC_E_INVAL;
+    const int64_t n = (int64_t)hd.pos.size();
+    hd.plan.resize(cycles);
+    for (int32_t i = 0; i < cycles; ++i) hd.plan[i] = n / cycles + (i < n % cycles ? 1 : 0);
+    hd.ticks = 0;
+    resv_active.insert(h);
+    return TC_OK;
+}
+
+tc_status Pool::reserve_tick() {
+    for (tc_handle h : resv_active) {           // issue order (std::set)
+        HandleRec &hd = handles[h];
+        hd.ticks += 1;
+        int64_t target = 0;
+        for (int32_t i = 0; i < hd.ticks && i < (int32_t)hd.plan.size(); ++i) target += hd.plan[i];
+        const int64_t want = target - (int64_t)hd.resv.size();
+        const int64_t uc = alloc.unclaimed(hd.cls);
+        const int64_t headroom = std::max<int64_t>(0, alloc.nfree - alloc.unclaimed_sum());
+        const int64_t k = std::min({want, alloc.nfree, uc + headroom});
+        if (k <= 0) continue;
+        const int64_t r = BlockAllocator::plan(hd.cls, k, alloc.nfree, alloc.reserved, alloc.claimed);
+        if (r < 0) continue;                     // cannot happen: k <= the largest admissible request
+        std::vector<int32_t> ids(k);
+        alloc.take_lowest(k, ids.data());
+        alloc.claimed[hd.cls] += r;
+        for (int32_t b : ids) {
+            alloc.state[b] = kReserved;
+            hd.resv.push_back(b);
+        }
+        n_reserved += k;
+    }
+    return TC_OK;
+}
+
+tc_status Pool::reserve_cancel(tc_handle h) {
+    auto it = handles.find(h);
+    if (it == handles.end() || it->second.state != kOffloaded) return TC_E_HANDLE;
+    HandleRec &hd = it->second;
+    for (int32_t b : hd.resv) {
+        alloc.state[b] = kFree;
+        alloc.set_free(b);
+    }
+    const int64_t k = (int64_t)hd.resv.size();
+    alloc.claimed[hd.cls] -= std::min(k, alloc.claimed[hd.cls]);
+    n_reserved -= k;
+    hd.resv.clear();
+    hd.plan.clear();
+    hd.ticks = 0;
+    resv_active.erase(h);
     return TC_OK;
 }
 
@@ -613,6 +864,8 @@ tc_status Pool::sync() {
         if (cuda_dead) return TC_E_CUDA;
         TC_CUDA(cudaStreamSynchronize(s_up), "sync upload stream");
         TC_CUDA(cudaStreamSynchronize(s_off), "sync offload stream");
+        TC_CUDA(cudaStreamSynchronize(s_up_k), "sync upload aux stream");
+        TC_CUDA(cudaStreamSynchronize(s_off_k), "sync offload aux stream");
         for (cudaStream_t f : foreign) TC_CUDA(cudaStreamSynchronize(f), "sync caller stream");
         spans_collect();
     }

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <set>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -14,7 +15,7 @@
 
 namespace tc {
 
-enum BlockState : uint8_t { kFree = 0, kAlloc = 1, kPending = 2 };
+enum BlockState : uint8_t { kFree = 0, kAlloc = 1, kPending = 2, kReserved = 3 };
 enum HandleState : int32_t { kOffloaded = 1, kUploaded = 2 };
 
 // Lowest-free-id bitmap allocator state + Space-Scheduler partition counters (SURVEY.md §8(c) ops 1-3).
@@ -61,6 +62,9 @@ struct HandleRec {
     std::vector<int64_t> slots;
     int32_t state = kOffloaded;
     int32_t ev = -1;                 // event of its latest transfer, -1 = completed / none
+    std::vector<int64_t> plan;       // gradual reservation: chunk per tick (empty = none active)
+    int32_t ticks = 0;
+    std::vector<int32_t> resv;       // destination blocks claimed so far, in claim order
 };
 
 struct Pool {
@@ -82,6 +86,9 @@ struct Pool {
 
     // streams / events
     cudaStream_t s_up = nullptr, s_off = nullptr, s_compute = nullptr;
+    cudaStream_t s_up_k = nullptr, s_off_k = nullptr;   // staged mode: device-side kernels of each direction
+    int64_t piece_bytes = 32ll << 20;                   // staged pipeline granularity
+    bool use_batch_memcpy = true;
     cudaEvent_t ev_compute = nullptr;
     std::vector<cudaStream_t> foreign;       // caller streams used by the device tier
     std::vector<cudaEvent_t> events;         // event pool
@@ -93,7 +100,8 @@ struct Pool {
 
     // transfer modes
     int32_t mode_d2h = TC_XFER_DIRECT, mode_h2d = TC_XFER_DIRECT;
-    int ctas_d2h = 0, ctas_h2d = 0, ctas_dev = 0, threads = 256;
+    // launch config per path: [0] direct D2H, [1] direct H2D, [2] device tier + staged kernels
+    int ctas[3] = {0, 0, 0}, nthreads[3] = {256, 256, 256}, variant[3] = {0, 0, 0};
 
     // bookkeeping
     BlockAllocator alloc;
@@ -136,10 +144,41 @@ struct Pool {
     tc_status offload_batch(int32_t na, const int32_t *agents, const int64_t *offsets, const int32_t *ids,
                             tc_handle *out);
     tc_status upload_batch(int32_t nh, const tc_handle *hs, const int64_t *offsets, int32_t *out_ids);
+    tc_status cycle(int32_t nh, const tc_handle *hs, const int64_t *up_off, int32_t *out_ids, int32_t na,
+                    const int32_t *ags, const int64_t *off_off, const int32_t *ids, tc_handle *out_h);
+    struct OffPlan {
+        int32_t na = 0;
+        const int32_t *ags = nullptr, *ids = nullptr;
+        const int64_t *off = nullptr;
+        std::vector<XferDesc> desc;
+        std::vector<int64_t> slot_of;
+    };
+    struct UpPlan {
+        int32_t nh = 0;
+        const tc_handle *hs = nullptr;
+        const int64_t *off = nullptr;
+        std::vector<HandleRec *> hr;
+        std::vector<int64_t> rr, need;
+        int64_t n_fresh = 0;
+        std::vector<int32_t> dst;
+        std::vector<XferDesc> desc;
+        std::vector<int64_t> slot_of;
+    };
+    tc_status plan_offload(OffPlan &P, int32_t na, const int32_t *ags, const int64_t *off, const int32_t *ids);
+    tc_status offload_waits(const OffPlan &P);
+    void commit_offload(const OffPlan &P, int32_t ev, tc_handle *out);
+    tc_status plan_upload(UpPlan &P, int32_t nh, const tc_handle *hs, const int64_t *off);
+    tc_status upload_waits(const UpPlan &P);
+    void commit_upload(const UpPlan &P, int32_t ev, int32_t *out_ids);
     tc_status query(tc_handle h, bool wait);
     tc_status stream_wait(tc_handle h, cudaStream_t s);
     tc_status sync();
     tc_status fill(uint64_t seed);
+    tc_status reserve_begin(tc_handle h, int32_t cycles);
+    tc_status reserve_tick();
+    tc_status reserve_cancel(tc_handle h);
+    std::set<tc_handle> resv_active;         // handles with an active gradual reservation, issue order
+    int64_t n_reserved = 0;
     tc_status device_tier(bool gather, const int32_t *ids, int64_t n, void *ext, cudaStream_t s);
 
     // helpers
@@ -148,6 +187,26 @@ struct Pool {
     char *ring_alloc(int64_t bytes, char **dev_ptr);
     tc_status enqueue_xfer(bool gather, int32_t mode, const std::vector<XferDesc> &desc,
                            const std::vector<int64_t> &slot_of, cudaStream_t s);
+    // two-phase transfer job (see runtime.cpp)
+    struct XferJob {
+        bool gather = false, ring_reuse = false;
+        int32_t mode = TC_XFER_DIRECT;
+        const std::vector<XferDesc> *desc = nullptr;
+        const std::vector<int64_t> *slot_of = nullptr;
+        cudaStream_t s = nullptr, sk = nullptr;
+        int64_t n = 0, pb = 1, R = 1, npieces = 0;
+        char *stg = nullptr;
+        std::vector<int32_t> ev;
+    };
+    tc_status xfer_init(XferJob &j, bool gather, int32_t mode, const std::vector<XferDesc> *desc,
+                        const std::vector<int64_t> *slot_of, cudaStream_t s);
+    tc_status xfer_phase_a(XferJob &j);
+    tc_status xfer_phase_b(XferJob &j);
+    tc_status xfer_copy(XferJob &j, int64_t a, int64_t b, char *base);
+    tc_status xfer_kernel(XferJob &j, int64_t a, int64_t b, char *base);
+    tc_status ev_rec(cudaStream_t st, int32_t *out);
+    std::vector<void *> cp_dst, cp_src;
+    std::vector<size_t> cp_size;
     tc_status table_push(int32_t a, int64_t pos0, int64_t n);
 };
 

@@ -29,6 +29,8 @@ class SetModel:
         self.nh = 0
         self.prov = {b: b for b in range(N)}   # physical block -> original content id
         self.hprov = {}
+        self.rplan = {}                  # handle -> [chunks, ticks] of an active gradual reservation
+        self.rsv = {}                    # handle -> destination ids claimed so far
 
     def _take(self, c, n):
         unc = [max(0, self.res[x] - self.clm[x]) for x in range(len(self.res))]
@@ -79,7 +81,10 @@ class SetModel:
         if h not in self.live:
             raise Fail(HANDLE)
         a, c, pos, slots = self.live[h]
-        got = self._take(c, len(pos))
+        mine = self.rsv.get(h, [])
+        got = list(mine) + (self._take(c, len(pos) - len(mine)) if len(pos) > len(mine) else [])
+        self.rsv.pop(h, None)
+        self.rplan.pop(h, None)
         for p, s, b in zip(pos, slots, got):
             self.prov[b] = self.hprov[s]
             self.own[b] = (a, p)
@@ -88,6 +93,38 @@ class SetModel:
         del self.live[h]
         self.dead.add(h)
         return got
+
+    def begin(self, h, cyc):
+        if h not in self.live:
+            raise Fail(HANDLE)
+        if cyc < 1 or h in self.rplan or self.rsv.get(h):
+            raise Fail(INVAL)
+        n = len(self.live[h][2])
+        q, m = divmod(n, cyc)
+        self.rplan[h] = [[q + 1] * m + [q] * (cyc - m), 0]
+        self.rsv[h] = []
+
+    def tick(self):
+        for h in sorted(self.rplan):
+            chunks, t = self.rplan[h]
+            t += 1
+            self.rplan[h][1] = t
+            c = self.live[h][1]
+            want = sum(chunks[:t]) - len(self.rsv[h])
+            unc = [max(0, self.res[x] - self.clm[x]) for x in range(len(self.res))]
+            room = max(0, len(self.free) - sum(unc))
+            k = min(want, len(self.free), unc[c] + room)
+            if k > 0:
+                self.rsv[h] += self._take(c, k)
+
+    def cancel(self, h):
+        if h not in self.live:
+            raise Fail(HANDLE)
+        mine = self.rsv.pop(h, [])
+        self.rplan.pop(h, None)
+        self.free.update(mine)
+        c = self.live[h][1]
+        self.clm[c] = max(0, self.clm[c] - len(mine))
 
     def sync(self):
         for c, ids in self.pend:

@@ -45,7 +45,8 @@ def meta_pool(N, S, ncls=N_CLASSES, max_bpa=4096, L=1, H=2, D=64):
 
 
 def stats_view(s):
-    return {k: s[k] for k in ("free", "alloc", "pending", "host_free", "host_used", "reserved", "claimed")}
+    return {k: s[k] for k in ("free", "alloc", "pending", "reserved_blocks", "host_free", "host_used", "reserved",
+                              "claimed")}
 
 
 def replay_both(ops, N, S, ncls=N_CLASSES, max_bpa=4096):
@@ -75,7 +76,8 @@ def test_fuzz_scripts_match_oracle(seed):
     rng = np.random.default_rng(seed)
     N = int(rng.choice([8, 24, 64]))
     S = int(rng.choice([4, 10, 32]))
-    ops = fuzz_script(seed, n_ops=150, n_agents=3, n_classes=2, N=N, max_alloc=int(rng.choice([2, 6, 12])))
+    ops = fuzz_script(seed, n_ops=150, n_agents=3, n_classes=2, N=N, max_alloc=int(rng.choice([2, 6, 12])),
+                      gradual=seed % 2 == 1)
     replay_both(ops, N, S, ncls=2, max_bpa=int(rng.choice([8, 4096])))
 
 

@@ -22,8 +22,9 @@ from workloads.configs import CONFIGS  # noqa: E402
 from workloads.replay import Replayer  # noqa: E402
 from workloads.scripts import N_CLASSES, build_script, c1_worked_example, fuzz_script  # noqa: E402
 
-MODES = {"direct": (tcb.XFER_DIRECT, tcb.XFER_DIRECT), "staged": (tcb.XFER_STAGED, tcb.XFER_STAGED),
-         "mixed": (tcb.XFER_DIRECT, tcb.XFER_STAGED)}
+MODES = {"direct": (tcb.XFER_DIRECT, tcb.XFER_DIRECT, 0), "staged": (tcb.XFER_STAGED, tcb.XFER_STAGED, 0),
+         "mixed": (tcb.XFER_DIRECT, tcb.XFER_STAGED, 0), "direct_tma": (tcb.XFER_DIRECT, tcb.XFER_DIRECT, 1),
+         "staged_tma": (tcb.XFER_STAGED, tcb.XFER_STAGED, 1)}
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -34,9 +35,11 @@ def _cuda():
 
 def dev_pool(L, H, D, N, S, mode="direct", ncls=N_CLASSES, max_bpa=4096, seed=1, rank=0, world=1, staging=0,
              dtype="bf16", T=16):
-    d2h, h2d = MODES[mode]
+    d2h, h2d, variant = MODES[mode]
     p = tcb.Pool(L, H, D, T, dtype, N, device=0, shard_rank=rank, shard_world=world, host_slots=S, n_classes=ncls,
                  max_agents=1024, max_blocks_per_agent=max_bpa, xfer_d2h=d2h, xfer_h2d=h2d, staging_bytes=staging)
+    for path in range(3):
+        p.set_launch_config(path, 0, 256, variant)
     p.fill(seed)
     return p
 
@@ -50,7 +53,7 @@ def compare_full(o: OraclePool, c: tcb.Pool, where=""):
     for a, ag in o.agents.items():
         assert tab[a, :len(ag.table)].tolist() == ag.table, (where, a)
     so, sc = o.stats(), c.stats()
-    for k in ("free", "alloc", "pending", "host_free", "host_used", "reserved", "claimed"):
+    for k in ("free", "alloc", "pending", "reserved_blocks", "host_free", "host_used", "reserved", "claimed"):
         assert so[k] == sc[k], (where, k)
 
 
@@ -101,7 +104,7 @@ GEOMS = [  # (L, H, D, N, S, T): ragged chunk counts vs CTA ranges, 4 KiB .. 32 
 def test_fuzz_scripts_bytes(mode, gi):
     L, H, D, N, S, T = GEOMS[gi]
     for seed in range(3):
-        ops = fuzz_script(seed + 10 * gi, n_ops=90, n_agents=3, n_classes=2, N=N)
+        ops = fuzz_script(seed + 10 * gi, n_ops=90, n_agents=3, n_classes=2, N=N, gradual=seed == 2)
         run_script(ops, L, H, D, N, S, mode, ncls=2, seed=seed + 1, staging=(3 * 2 * L * T * H * D * 2), T=T)
 
 
@@ -117,9 +120,10 @@ def test_fill_kernel_matches_generator_sharded():
             c.close()
 
 
-def test_device_tier_equals_numpy_take():
+@pytest.mark.parametrize("variant", [0, 1])
+def test_device_tier_equals_numpy_take(variant):
     L, H, D, N = 4, 4, 128, 64
-    c = dev_pool(L, H, D, N, 4, seed=9)
+    c = dev_pool(L, H, D, N, 4, seed=9, mode="direct_tma" if variant else "direct")
     pool0 = content.pool_bytes(9, L, N, 16, H, D)
     rng = np.random.default_rng(0)
     ids = rng.choice(N, size=23, replace=False).astype(np.int32)
@@ -177,7 +181,7 @@ def test_full_size_config_parity(name, world):
     cfg = CONFIGS[name]
     rank = world - 1 if world > 1 else 0
     S = cfg.host_slots()
-    ops = build_script(cfg, 8)
+    ops = build_script(cfg, 8, combined=True)          # tc_cycle per scheduling cycle, as bench.py times it
     o = OraclePool(cfg.N, S, max_agents=1024, max_blocks_per_agent=cfg.max_blocks_per_agent,
                    store=ProvStore(cfg.N, S))
     c = tcb.Pool(cfg.L, cfg.H, cfg.D, cfg.T, cfg.dtype, cfg.N, device=0, shard_rank=rank, shard_world=world,
@@ -189,8 +193,8 @@ def test_full_size_config_parity(name, world):
         a, b = ro.step(op), rc.step(op)
         assert a == b, (i, op)
         assert a[0] == 0, (i, op)
-        if op[0] in ("upload_batch", "upload") and a[1]:
-            for ids in (a[1] if op[0] == "upload_batch" else [a[1]]):
+        if op[0] == "cycle" and a[1]:
+            for ids in a[1][0]:
                 touched.update(ids)
     c.sync()
     tab = c.table_tensor().cpu().numpy()

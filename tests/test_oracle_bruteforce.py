@@ -20,6 +20,8 @@ ALPHABET = ([("alloc", a, n) for a in (A, B) for n in (1, 2)]
             + [("upload", w) for w in ("oldest", "newest")]
             + [("sync",)] + [("reserve", 0, n) for n in (0, 2)] + [("agent_free", a) for a in (A, B)])
 assert len(ALPHABET) == 15
+# NEXT-1 gradual reservation: begin a 2-tick reservation for the oldest live handle; one scheduling tick
+ALPHABET_R = ALPHABET + [("reserve_begin", 2), ("tick",)]
 
 
 def sel_ids(table, sel):
@@ -44,6 +46,11 @@ def run_oracle(p: OraclePool, op):
             return 0, p.reserve(op[1], op[2])
         if k == "agent_free":
             return 0, p.agent_free(op[1])
+        if k == "reserve_begin":
+            live = sorted(h for h, x in p.handles.items() if x.state == OFFLOADED)
+            return 0, p.reserve_begin(live[0] if live else 0, op[1])
+        if k == "tick":
+            return 0, p.reserve_tick()
     except OracleError as e:
         return e.status, None
     raise AssertionError(op)
@@ -66,6 +73,11 @@ def run_model(m: SetModel, op):
             return 0, m.reserve(op[1], op[2])
         if k == "agent_free":
             return 0, m.agent_free(op[1])
+        if k == "reserve_begin":
+            live = sorted(m.live)
+            return 0, m.begin(live[0] if live else 0, op[1])
+        if k == "tick":
+            return 0, m.tick()
     except Fail as e:
         return e.status, None
     raise AssertionError(op)
@@ -74,6 +86,9 @@ def run_model(m: SetModel, op):
 def compare(p: OraclePool, m: SetModel, pool0, where):
     s = p.stats()
     assert (s["free"], s["alloc"], s["pending"]) == m.counts(), where
+    assert s["reserved_blocks"] == sum(len(v) for v in m.rsv.values()), where
+    assert {h: list(x.resv) for h, x in p.handles.items() if x.state == OFFLOADED and x.resv} == \
+        {h: v for h, v in m.rsv.items() if v}, where
     assert p.block_table(A) == m.tab[A] and p.block_table(B) == m.tab[B], where
     assert p.reserved == m.res and p.claimed == m.clm, where
     assert p.slot_free == m.stack and p.released_slots == m.back, where
@@ -93,10 +108,13 @@ def key(p: OraclePool, m: SetModel):
             tuple(p.slot_free), tuple(p.released_slots), tuple(map(tuple, (x[1] for x in p.pending_dev))),
             tuple((h, x.state, tuple(x.pos), tuple(x.slots)) for h, x in p.handles.items()), p.next_handle,
             tuple(sorted(m.free)), tuple(sorted(m.prov.items())), tuple(sorted(m.hprov.items())),
-            tuple(m.stack), tuple(m.back), tuple(sorted(m.live)))
+            tuple(m.stack), tuple(m.back), tuple(sorted(m.live)),
+            tuple((h, tuple(x.plan), x.ticks, tuple(x.resv)) for h, x in p.handles.items()),
+            tuple(sorted((h, tuple(v[0]), v[1]) for h, v in m.rplan.items())),
+            tuple(sorted((h, tuple(v)) for h, v in m.rsv.items())))
 
 
-def explore(N, S, depth):
+def explore(N, S, depth, alphabet=ALPHABET):
     pool0 = content.pool_bytes(9, 1, N, 1, 1, 8)          # C = 16 bytes per chunk
     p = OraclePool(N, S, n_classes=2, store=BytesStore(pool0, S))
     m = SetModel(N, S)
@@ -113,7 +131,7 @@ def explore(N, S, depth):
         if k in seen:
             return
         seen.add(k)
-        for op in ALPHABET:
+        for op in alphabet:
             p2, m2 = copy.deepcopy(p), copy.deepcopy(m)
             ro, rm = run_oracle(p2, op), run_model(m2, op)
             nodes[0] += 1
@@ -129,6 +147,12 @@ def explore(N, S, depth):
 @pytest.mark.parametrize("N,S,depth", [(4, 3, 5), (6, 4, 5), (5, 2, 6)])
 def test_bruteforce_vs_set_model(N, S, depth):
     n, states = explore(N, S, depth)
+    assert n > 1000 and states > 100
+
+
+@pytest.mark.parametrize("N,S,depth", [(4, 3, 5), (6, 4, 5)])
+def test_bruteforce_gradual_reservation(N, S, depth):
+    n, states = explore(N, S, depth, ALPHABET_R)
     assert n > 1000 and states > 100
 
 

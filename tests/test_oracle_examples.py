@@ -204,3 +204,68 @@ def test_block_states_and_location_flags():
     assert p.blk_state[t[0]] == ALLOC
     p.sync()
     assert p.blk_state[t[1]] == FREE
+
+
+# ------------------------------------------------------------------------------------------- NEXT-1 gradual reservation
+def _offloaded(N, n, S=None, cls=0):
+    p = OraclePool(N, S or max(n, 1))
+    p.agent_add(0, cls); p.agent_add(1, 1)
+    p.alloc(0, n)
+    h = p.offload(0, p.block_table(0))
+    p.sync()
+    return p, h
+
+
+def test_spec_gradual_reservation_chunks():
+    g = gold("spec_gradual_reservation.json")
+    for key in ("even_split", "largest_first"):
+        e = g[key]
+        p, h = _offloaded(256, e["n"])
+        p.reserve_begin(h, e["cycles"])
+        got = []
+        for _ in range(e["cycles"]):
+            before = p.reserve_info(h)[0]
+            p.reserve_tick()
+            got.append(p.reserve_info(h)[0] - before)
+        assert got == e["expect_chunks"], key
+        assert p.reserve_info(h) == (e["n"], e["n"])
+
+
+def test_spec_gradual_reservation_total_shortfall_then_stall():
+    p, h = _offloaded(16, 8)
+    p.alloc(1, 16)                                    # device_free = 0 at every tick
+    p.reserve_begin(h, 4)
+    for _ in range(4):
+        p.reserve_tick()
+    assert p.reserve_info(h) == (0, 8)                # readiness 0 at the deadline
+    assert status_of(p.upload, h) == E_NOBLOCKS       # falls back to the stall path
+
+
+def test_spec_reservation_covers_demand():
+    e = gold("spec_gradual_reservation.json")["reservation_covers_demand"]
+    n = e["n"]
+    p, h = _offloaded(2 * n, n)
+    p.reserve_begin(h, 4)
+    for _ in range(4):
+        p.reserve_tick()
+    p.alloc(1, p.stats()["free"])                     # now device_free = 0
+    assert p.stats()["free"] == 0
+    new = p.upload(h)                                 # no allocation stall
+    assert len(new) == n and p.stats()["reserved_blocks"] == 0
+
+
+def test_gradual_reservation_shortfall_carries_and_cancel():
+    p, h = _offloaded(32, 12)
+    p.alloc(1, 18)                                    # free = 2 (12 pending retired -> 14 free; 18 taken... )
+    free0 = p.stats()["free"]
+    p.reserve_begin(h, 3)                             # chunks 4/4/4
+    p.reserve_tick()
+    assert p.reserve_info(h)[0] == min(4, free0)
+    p.agent_free(1)                                   # blocks come back: the shortfall carries
+    p.reserve_tick()
+    assert p.reserve_info(h)[0] == 8
+    before = p.stats()
+    p.reserve_cancel(h)
+    after = p.stats()
+    assert after["free"] == before["free"] + 8 and after["reserved_blocks"] == 0
+    assert p.upload(h) == list(range(12))             # plain lowest-free upload after the cancel

@@ -3,7 +3,7 @@ reductions (numpy.take / fancy-index assignment), over seeded random scripts."""
 import numpy as np
 import pytest
 
-from oracle import ALLOC, FREE, PENDING, BytesStore, OraclePool, ProvStore
+from oracle import ALLOC, FREE, PENDING, RESERVED, BytesStore, OraclePool, ProvStore
 from oracle.pool import OFFLOADED
 from workloads import content
 from workloads.configs import C2, C3
@@ -22,7 +22,9 @@ def check_invariants(p: OraclePool, prev_sound: bool) -> bool:
     N, S = p.N, p.S
     st = p.blk_state
     # conservation |FREE| + |ALLOC| + |PENDING| = N
-    assert (st == FREE).sum() + (st == ALLOC).sum() + (st == PENDING).sum() == N
+    assert (st == FREE).sum() + (st == ALLOC).sum() + (st == PENDING).sum() + (st == RESERVED).sum() == N
+    # gradually reserved blocks are exactly the live handles' claim lists
+    assert set(np.flatnonzero(st == RESERVED).tolist()) == {b for h in p.handles.values() for b in h.resv}
     # host conservation: slots in use by live handles + released-not-returned + free list = S
     live = [s for h in p.handles.values() if h.state == OFFLOADED for s in h.slots]
     assert len(live) + len(p.released_slots) + len(p.slot_free) == S
@@ -52,7 +54,7 @@ def test_invariants_and_round_trip_on_fuzz(seed):
     N, S = 24, 10
     p, pool0 = make(N, S, seed)
     r = Replayer(p)
-    ops = fuzz_script(seed, n_ops=120, n_agents=3, n_classes=2, N=N)
+    ops = fuzz_script(seed, n_ops=120, n_agents=3, n_classes=2, N=N, gradual=seed % 2 == 1)
     snap_at_offload = {}           # handle -> bytes of its blocks at offload time, [n][L][2][C]
     sound = True
     for op in ops:
@@ -60,14 +62,14 @@ def test_invariants_and_round_trip_on_fuzz(seed):
         live_before = {h for h, x in p.handles.items() if x.state == OFFLOADED}
         pool_before = p.store.pool.copy()
         st, out = r.step(op)
-        if st == 0 and op[0] in ("offload", "offload_batch"):
+        if st == 0 and op[0] in ("offload", "offload_batch", "cycle"):
             for h in range(hbefore, p.next_handle):
                 hd = p.handles[h]
                 # the gathered slots hold exactly the source blocks' bytes as they were before the offload
                 snap_at_offload[h] = np.stack([p.store.host[s].copy() for s in hd.slots])
-        if st == 0 and op[0] in ("upload", "upload_batch"):
+        if st == 0 and op[0] in ("upload", "upload_batch", "cycle"):
             done = sorted(h for h in live_before if p.handles[h].state != OFFLOADED)
-            news = [out] if op[0] == "upload" else out
+            news = [out] if op[0] == "upload" else (out[0] if op[0] == "cycle" else out)
             assert len(done) == len(news)
             touched = set()
             for h in done:

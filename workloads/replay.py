@@ -65,10 +65,30 @@ class Replayer:
                 out = [list(x) for x in p.upload_batch(hs)]
                 for a in op[1]:
                     self.handles[a].popleft()
+            elif kind == "cycle":                # ("cycle", [upload agents], [(agent, sel), ...])
+                items = [(a, self._ids(a, sel)) for a, sel in op[2]]       # resolved on pre-cycle tables
+                taken = defaultdict(int)
+                hs = []
+                for a in op[1]:
+                    q = self.handles.get(a, ())
+                    hs.append(q[taken[a]] if taken[a] < len(q) else 0)
+                    taken[a] += 1
+                news, out_h = p.cycle(hs, items)
+                for a in op[1]:
+                    self.handles[a].popleft()
+                for (a, _), h in zip(op[2], out_h):
+                    self.handles[a].append(h)
+                out = ([list(x) for x in news], list(out_h))
             elif kind == "sync":
                 p.sync(); out = None
             elif kind == "agent_free":
                 p.agent_free(op[1]); out = None
+            elif kind == "reserve_begin":        # gradual reservation for the agent's oldest handle (NEXT-1)
+                p.reserve_begin(self._handle(op[1]), op[2]); out = None
+            elif kind == "tick":
+                p.reserve_tick(); out = None
+            elif kind == "reserve_cancel":
+                p.reserve_cancel(self._handle(op[1])); out = None
             else:
                 raise ValueError(f"unknown op {op!r}")
             return 0, out

@@ -86,8 +86,9 @@ class CycleGen:
     """Steady-state scheduling cycles: uploads of agents whose FC is over, then offloads of agents entering an FC
     (P:645-647 order), then a sync.  Deterministic given the config seed."""
 
-    def __init__(self, cfg: Config, agents: list, rng: np.random.Generator | None = None):
+    def __init__(self, cfg: Config, agents: list, rng: np.random.Generator | None = None, combined: bool = False):
         self.cfg = cfg
+        self.combined = combined           # emit one ("cycle", ups, offs) op per cycle (tc_cycle)
         self.rng = rng if rng is not None else np.random.default_rng(cfg.seed + 1000)
         self.running = deque(agents)
         self.stalled: deque = deque()      # (agent, cycle offloaded)
@@ -99,13 +100,16 @@ class CycleGen:
         due = []
         while self.stalled and self.stalled[0][1] <= self.t - cfg.stall_cycles and len(due) < cfg.per_cycle:
             due.append(self.stalled.popleft()[0])
-        if due:
-            ops.append(("upload_batch", due))
         off = []
         for _ in range(min(cfg.per_cycle, len(self.running))):
             off.append(self.running.popleft())
-        if off:
-            ops.append(("offload_batch", [(a, "all") for a in off]))
+        if self.combined and (due or off):
+            ops.append(("cycle", due, [(a, "all") for a in off]))
+        else:
+            if due:
+                ops.append(("upload_batch", due))
+            if off:
+                ops.append(("offload_batch", [(a, "all") for a in off]))
         for a in off:
             self.stalled.append((a, self.t))
         self.running.extend(due)
@@ -114,9 +118,9 @@ class CycleGen:
         return ops
 
 
-def build_script(cfg: Config, n_cycles: int) -> list:
+def build_script(cfg: Config, n_cycles: int, combined: bool = False) -> list:
     ops, agents, _ = setup_ops(cfg)
-    gen = CycleGen(cfg, agents)
+    gen = CycleGen(cfg, agents, combined=combined)
     for _ in range(n_cycles):
         ops.extend(gen.next_cycle())
     return ops
@@ -132,12 +136,12 @@ def c1_worked_example() -> list:
 
 
 def fuzz_script(seed: int, n_ops: int = 60, n_agents: int = 3, n_classes: int = 2, N: int = 64,
-                max_alloc: int = 6, p_err: float = 0.05) -> list:
+                max_alloc: int = 6, p_err: float = 0.05, gradual: bool = False) -> list:
     """Random op mix for small pools, including error paths (bad ids, double uploads, over-quota, BUSY frees)."""
     rng = np.random.default_rng(seed)
     ops = [("agent_add", a, a % n_classes) for a in range(n_agents)]
     kinds = ["alloc", "alloc", "offload", "offload_some", "upload", "sync", "reserve", "agent_free",
-             "offload_batch", "upload_batch"]
+             "offload_batch", "upload_batch", "cycle"] + (["reserve_begin", "tick", "tick", "reserve_cancel"] if gradual else [])
     for _ in range(n_ops):
         k = kinds[rng.integers(len(kinds))]
         a = int(rng.integers(n_agents))
@@ -158,9 +162,19 @@ def fuzz_script(seed: int, n_ops: int = 60, n_agents: int = 3, n_classes: int = 
         elif k == "offload_batch":
             bs = sorted(set(int(x) for x in rng.integers(n_agents, size=2)))
             ops.append(("offload_batch", [(b, "all") for b in bs]))
-        else:
+        elif k == "upload_batch":
             bs = sorted(set(int(x) for x in rng.integers(n_agents, size=2)))
             ops.append(("upload_batch", bs))
+        elif k == "cycle":
+            ups = sorted(set(int(x) for x in rng.integers(n_agents, size=int(rng.integers(0, 3)))))
+            offs = sorted(set(int(x) for x in rng.integers(n_agents, size=int(rng.integers(0, 3)))))
+            ops.append(("cycle", ups, [(b, "all") for b in offs]))
+        elif k == "reserve_begin":
+            ops.append(("reserve_begin", a, int(rng.integers(1, 4))))
+        elif k == "tick":
+            ops.append(("tick",))
+        else:
+            ops.append(("reserve_cancel", a))
         if rng.random() < p_err:
             ops.append(("alloc", 99, 1))              # unknown agent -> E_INVAL on both sides
     ops.append(("sync",))
