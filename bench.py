@@ -224,6 +224,7 @@ def run_ours(args):
         cycle()
     pool.timing(True)
     pool.timing(True)                          # reset accumulators
+    pool.timeline_arm(200000)
     launches0 = pool.stats()["kernel_launches"]
     memcpy0 = pool.stats()["memcpy_calls"]
     if dist is not None:
@@ -258,6 +259,7 @@ def run_ours(args):
     t_wall = time.perf_counter() - t_wall0
     clk = clocks.stop()
     tim = pool.timing(False)
+    tl_summary = timeline_summary(pool.timeline(200000))
     launches = pool.stats()["kernel_launches"] - launches0
 
     my = torch.tensor([sum(dev_ms), sum(host_ms), bytes_up + bytes_off, blocks, t_wall], dtype=torch.float64,
@@ -347,6 +349,7 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "memcpy_calls_per_step": (stats["memcpy_calls"] - memcpy0) / n_steps,
         "kernels": kern,
+        "timeline": tl_summary,
         "hostlink_peak": link,
         "roofline": roof,
         "roofline_link": link_roof,
@@ -361,6 +364,26 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier(); dist.destroy_process_group()
+
+
+def timeline_summary(spans):
+    """Per sync interval (= step): when each kind of span first starts and last ends, relative to the step's first
+    span; averaged over steps.  Shows how early each host-link direction starts and where the step's tail is."""
+    by = {}
+    for sync, kind, t0, t1, _ in spans:
+        d = by.setdefault(sync, {})
+        a, b = d.get(kind, (t0, t1))
+        d[kind] = (min(a, t0), max(b, t1))
+    if not by:
+        return None
+    kinds = sorted({k for d in by.values() for k in d})
+    out = {}
+    for k in kinds:
+        v = [d[k] for d in by.values() if k in d]
+        out[k] = {"first_start_ms": statistics.mean(x[0] for x in v), "last_end_ms": statistics.mean(x[1] for x in v)}
+    out["step_span_ms"] = statistics.mean(max(x[1] for x in d.values()) for d in by.values())
+    out["steps"] = len(by)
+    return out
 
 
 def device_tier_bench(torch, pool, cfg, dev, hbm, hbm_src):

@@ -196,6 +196,16 @@ typedef struct tc_timing_t {
 /* enable != 0 turns span recording on (off by default: zero overhead).  If out != NULL it receives the totals
    accumulated since the previous call, which are then reset. */
 tc_status tc_timing(tc_pool *p, int32_t enable, tc_timing_t *out);
+/* Per-span timeline (needs tc_timing enabled): kind as in tc_timing_t, start/end in ms relative to the first span
+   after the previous tc_sync, `sync` = index of the sync interval.  out == NULL arms recording of up to `cap`
+   records (clearing old ones); otherwise copies up to `cap` records to out, sets *n_out and clears. */
+typedef struct tc_span_t {
+    int64_t sync;
+    int32_t kind;
+    double start_ms, end_ms;
+    int64_t bytes;
+} tc_span_t;
+tc_status tc_timeline(tc_pool *p, int64_t cap, tc_span_t *out, int64_t *n_out);
 const char *tc_strerror(tc_status s);
 const char *tc_last_error(tc_pool *p);
 

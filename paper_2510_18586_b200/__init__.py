@@ -30,7 +30,7 @@ SYMBOLS = [
     "tc_agent_add", "tc_alloc", "tc_agent_free", "tc_offload", "tc_upload", "tc_offload_batch", "tc_upload_batch",
     "tc_cycle", "tc_reserve_begin", "tc_reserve_tick", "tc_reserve_cancel", "tc_reserve_info",
     "tc_query", "tc_wait", "tc_stream_wait", "tc_sync", "tc_block_table", "tc_block_table_dev", "tc_handle_info",
-    "tc_handle_host", "tc_stats", "tc_timing", "tc_strerror", "tc_last_error", "tc_gather_dev", "tc_scatter_dev",
+    "tc_handle_host", "tc_stats", "tc_timing", "tc_timeline", "tc_strerror", "tc_last_error", "tc_gather_dev", "tc_scatter_dev",
 ]
 
 
@@ -54,6 +54,11 @@ class PoolDesc(ctypes.Structure):
 
 class Timing(ctypes.Structure):
     _fields_ = [("ms", ctypes.c_double * 5), ("count", ctypes.c_int64 * 5), ("bytes", ctypes.c_int64 * 5)]
+
+
+class Span(ctypes.Structure):
+    _fields_ = [("sync", ctypes.c_int64), ("kind", ctypes.c_int32), ("start_ms", ctypes.c_double),
+                ("end_ms", ctypes.c_double), ("bytes", ctypes.c_int64)]
 
 
 TIMING_KINDS = ("offload_kernel", "upload_kernel", "device_kernel", "memcpy_d2h", "memcpy_h2d")
@@ -112,6 +117,7 @@ def _load() -> ctypes.CDLL:
         "tc_handle_host": (I32, [P, U64, I64, ctypes.POINTER(VP)]),
         "tc_stats": (I32, [P, ctypes.POINTER(Stats)]),
         "tc_timing": (I32, [P, I32, ctypes.POINTER(Timing)]),
+        "tc_timeline": (I32, [P, I64, ctypes.POINTER(Span), PI64]),
         "tc_strerror": (ctypes.c_char_p, [I32]),
         "tc_last_error": (ctypes.c_char_p, [P]),
         "tc_gather_dev": (I32, [P, PI32, I64, VP, VP]),
@@ -359,6 +365,18 @@ class Pool:
         t = Timing()
         self._check(lib.tc_timing(self._h, 1 if enable else 0, ctypes.byref(t)))
         return {k: (t.ms[i], t.count[i], t.bytes[i]) for i, k in enumerate(TIMING_KINDS)}
+
+    def timeline_arm(self, cap: int = 100000):
+        n = ctypes.c_int64()
+        self._check(lib.tc_timeline(self._h, cap, None, ctypes.byref(n)))
+
+    def timeline(self, cap: int = 100000) -> list:
+        """[(sync_index, kind_name, start_ms, end_ms, bytes), ...] recorded since timeline_arm()."""
+        buf = (Span * cap)()
+        n = ctypes.c_int64()
+        self._check(lib.tc_timeline(self._h, cap, buf, ctypes.byref(n)))
+        return [(buf[i].sync, TIMING_KINDS[buf[i].kind], buf[i].start_ms, buf[i].end_ms, buf[i].bytes)
+                for i in range(n.value)]
 
     def streams(self):
         up, off = ctypes.c_void_p(), ctypes.c_void_p()

@@ -2,6 +2,7 @@
 // exception containment around the runtime in runtime.cpp.  No C++ exception crosses this boundary.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <new>
 
@@ -323,6 +324,24 @@ tc_status tc_timing(tc_pool *p, int32_t enable, tc_timing_t *out) {
             *out = P.tacc;
             P.tacc = tc_timing_t{};
         }
+        return TC_OK;
+    }
+    TC_CATCH
+}
+
+tc_status tc_timeline(tc_pool *p, int64_t cap, tc_span_t *out, int64_t *n_out) {
+    TC_GUARD(p) {
+        if (!n_out) return TC_E_INVAL;
+        if (!out) {                                  // (re)arm: keep up to `cap` records from now on
+            P.timeline.clear();
+            P.timeline_cap = cap;
+            *n_out = 0;
+            return TC_OK;
+        }
+        const int64_t n = std::min<int64_t>(cap, (int64_t)P.timeline.size());
+        std::memcpy(out, P.timeline.data(), (size_t)n * sizeof(tc_span_t));
+        *n_out = n;
+        P.timeline.clear();
         return TC_OK;
     }
     TC_CATCH

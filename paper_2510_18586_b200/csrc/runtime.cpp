@@ -255,6 +255,11 @@ void Pool::spans_collect() {
             tacc.ms[sp.kind] += ms;
             tacc.count[sp.kind] += 1;
             tacc.bytes[sp.kind] += sp.bytes;
+            if (timeline.size() < (size_t)timeline_cap) {      // start/end relative to this sync interval's first span
+                float t0 = 0.f;
+                cudaEventElapsedTime(&t0, spans.front().a, sp.a);
+                timeline.push_back(tc_span_t{sync_count, sp.kind, (double)t0, (double)(t0 + ms), sp.bytes});
+            }
         }
         tev_free.push_back(sp.a);
         tev_free.push_back(sp.b);
@@ -868,6 +873,7 @@ tc_status Pool::sync() {
         TC_CUDA(cudaStreamSynchronize(s_off_k), "sync offload aux stream");
         for (cudaStream_t f : foreign) TC_CUDA(cudaStreamSynchronize(f), "sync caller stream");
         spans_collect();
+        ++sync_count;
     }
     for (auto &pc : pending_dev) {        // a4 retire in issue order (A10)
         for (int32_t b : pc.second) {

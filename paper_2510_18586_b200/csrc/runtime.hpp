@@ -128,6 +128,9 @@ struct Pool {
     tc_status span_begin(cudaStream_t s, cudaEvent_t *a);
     tc_status span_end(cudaStream_t s, int32_t kind, cudaEvent_t a, int64_t bytes);
     void spans_collect();
+    std::vector<tc_span_t> timeline;         // per-span records (tc_timeline), capped
+    int64_t timeline_cap = 0;
+    int64_t sync_count = 0;
 
     // counters / errors
     int64_t n_launch = 0, n_memcpy = 0, bytes_d2h = 0, bytes_h2d = 0;
