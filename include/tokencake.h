@@ -209,6 +209,55 @@ tc_status tc_timeline(tc_pool *p, int64_t cap, tc_span_t *out, int64_t *n_out);
 const char *tc_strerror(tc_status s);
 const char *tc_last_error(tc_pool *p);
 
+/* ---- NEXT-3: Time-Scheduler decision layer (§4.1-4.2), host-only -------------------------------- */
+/* FC-duration history of one (agent type, call label): EWMA t_hist after n_obs observations, cold-start estimate
+   from static analysis. */
+typedef struct tc_fc_stat { double t_hist; int64_t n_obs; double cold_start; } tc_fc_stat;
+/* Eq. 1: t_final = alpha*t_req + (1-alpha)*t_hist; t_req < 0 = no developer hint.  Before the first
+   observation: the hint if given, else the cold-start estimate. */
+double tc_fc_predict(const tc_fc_stat *s, double t_req, double alpha);
+/* Feed back an observed duration: first sets t_hist, then t_hist = beta*obs + (1-beta)*t_hist. */
+tc_status tc_fc_observe(tc_fc_stat *s, double observed_ms, double beta);
+/* T_transfer(n) = T_offload(n) + T_upload(n), linear in the block count. */
+typedef struct tc_xfer_model { double offload_ms_per_block, upload_ms_per_block, fixed_ms; } tc_xfer_model;
+double tc_transfer_ms(const tc_xfer_model *m, int64_t n_blocks);
+/* Calibrate the model from this pool's own measured transfers (needs tc_timing on and at least one tc_sync after
+   an offload and an upload; TC_E_BUSY otherwise) — replaces SPEC's paper-derived 60 ms / 4096 blocks. */
+tc_status tc_xfer_model_measure(tc_pool *p, tc_xfer_model *m);
+typedef struct tc_offload_decision {
+    int32_t offload;      /* 1 = offload */
+    int32_t match;        /* index of the best-fit waiting request, -1 = none */
+    double t_transfer, t_window, n_capacity;
+} tc_offload_decision;
+/* Alg. 1 ShouldOffload: retain if T_fc <= T_transfer; N_capacity = (T_fc - T_transfer) * v_throughput;
+   offload iff some waiting request's token demand fits (best fit = the largest that fits, earliest on ties). */
+tc_status tc_should_offload(int64_t n_blocks, double t_fc_ms, double t_transfer_ms, double v_tokens_per_s,
+                            const double *waiting_tokens, int64_t n_waiting, tc_offload_decision *out);
+typedef struct tc_upload_plan { int32_t immediate; double upload_start, reservation_deadline, predicted_finish; }
+    tc_upload_plan;
+/* Predictive upload: upload_start = call_start + t_final - upload_ms, gradual reservation ready lead_ms
+   before it; if that is before the offload can finish, upload immediately after it. */
+tc_status tc_plan_upload(double call_start, double t_final, double upload_ms, double offload_ms, double lead_ms,
+                         tc_upload_plan *out);
+
+/* ---- NEXT-4: Space-Scheduler partitions (§5), host-only ------------------------------------------ */
+double tc_static_priority(double w_static, int32_t node_depth, int32_t node_out_degree);
+/* time_wait * ln(max(tokens_req / max(time_wait, 1 ms), 1)) (clamp: DESIGN.md B7) */
+double tc_dynamic_priority(double time_wait_ms, double tokens_req);
+/* critical[t] = 1 for the top max(1, floor(ratio * n)) types by score, ties to the lower index (B6). */
+tc_status tc_select_critical(int32_t n_types, const double *scores, double critical_ratio, uint8_t *critical);
+typedef struct tc_partition_params {
+    double gpu_usage_high, gpu_usage_low, adjustment_step, reserve_ratio_max;   /* SPEC: 0.85, 0.50, 0.05, 0.40 */
+} tc_partition_params;
+/* Alg. 2 UpdateMemoryReservations: Phase 1 adjusts *total_reserve_ratio by usage/tot_blks (clamped to
+   [0, reserve_ratio_max]); Phase 2 reserve_num[t] = floor(final_ratio * R_total) for critical types (0 otherwise),
+   final_ratio = (usage_t/tot + score_t/S_total)/2, renormalised if they sum above 1 (B8). */
+tc_status tc_update_reservations(const tc_partition_params *pp, double *total_reserve_ratio, int64_t usage,
+                                 int64_t tot_blks, int32_t n_types, const uint8_t *critical, const double *scores,
+                                 const int64_t *type_usage, double *r_total, int64_t *reserve_num);
+/* Apply quotas to the pool's classes at once (tc_partition_reserve semantics, all-or-nothing, lazy shrink). */
+tc_status tc_apply_reservations(tc_pool *p, int32_t n, const int32_t *classes, const int64_t *reserve_num);
+
 /* ---- device tier (staged halves; NEXT-2 building block) ---------------------------------------------------- */
 /* Gather blocks ids[0..n) into a contiguous device buffer dst[n][L][2][C] (the HBM-bound KG1 kernel), or scatter
    src[n][L][2][C] into blocks ids[0..n) (KS1), on `cuda_stream` (NULL = the offload stream).  No allocator or

@@ -30,7 +30,12 @@ SYMBOLS = [
     "tc_agent_add", "tc_alloc", "tc_agent_free", "tc_offload", "tc_upload", "tc_offload_batch", "tc_upload_batch",
     "tc_cycle", "tc_reserve_begin", "tc_reserve_tick", "tc_reserve_cancel", "tc_reserve_info",
     "tc_query", "tc_wait", "tc_stream_wait", "tc_sync", "tc_block_table", "tc_block_table_dev", "tc_handle_info",
-    "tc_handle_host", "tc_stats", "tc_timing", "tc_timeline", "tc_strerror", "tc_last_error", "tc_gather_dev", "tc_scatter_dev",
+    "tc_handle_host", "tc_stats", "tc_timing", "tc_timeline", "tc_strerror", "tc_last_error", "tc_gather_dev",
+    "tc_scatter_dev",
+    # decision layers (paper_2510_18586_b200/sched.py binds them)
+    "tc_fc_predict", "tc_fc_observe", "tc_transfer_ms", "tc_xfer_model_measure", "tc_should_offload",
+    "tc_plan_upload", "tc_static_priority", "tc_dynamic_priority", "tc_select_critical", "tc_update_reservations",
+    "tc_apply_reservations",
 ]
 
 

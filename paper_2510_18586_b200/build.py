@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libtokencake.so")
-SOURCES = ["kernels.cu", "runtime.cpp", "capi.cpp"]
+SOURCES = ["kernels.cu", "runtime.cpp", "capi.cpp", "sched.cpp"]
 HEADERS = ["kernels.cuh", "runtime.hpp"]
 
 

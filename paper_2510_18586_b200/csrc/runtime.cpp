@@ -158,7 +158,8 @@ tc_status Pool::create(const tc_pool_desc &d) {
     TC_CUDA(cudaStreamCreateWithPriority(&s_off, cudaStreamNonBlocking, lo), "offload stream");
     TC_CUDA(cudaStreamCreateWithPriority(&s_up_k, cudaStreamNonBlocking, hi), "upload aux stream");
     TC_CUDA(cudaStreamCreateWithPriority(&s_off_k, cudaStreamNonBlocking, lo), "offload aux stream");
-    piece_bytes = env_int("TC_PIECE_KIB", 32768) * 1024ll;
+    piece_bytes = env_int("TC_PIECE_KIB", 256 * 1024) * 1024ll;
+    head_bytes = env_int("TC_HEAD_KIB", 4096) * 1024ll;
     use_batch_memcpy = env_int("TC_BATCH_MEMCPY", 1) != 0;
     TC_CUDA(cudaEventCreateWithFlags(&ev_compute, cudaEventDisableTiming), "event");
     const int64_t kv_bytes = (int64_t)L * 2 * N * C;
@@ -189,7 +190,7 @@ tc_status Pool::create(const tc_pool_desc &d) {
         cudaGetLastError(); ring_host = nullptr; return TC_E_OOM;
     }
     TC_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&ring_dev), ring_host, 0), "ring dev ptr");
-    staging_bytes = d.staging_bytes > 0 ? d.staging_bytes : (256ll << 20);
+    staging_bytes = d.staging_bytes > 0 ? d.staging_bytes : (1ll << 30);
     if (staging_bytes < B) staging_bytes = B;
     // AUTO: the copy-engine staged path measured faster than the SM direct path in both directions on B200
     // (profiles/r01_xfer_probe.json: alone 57.1 vs 52.6 GB/s D2H, 55.4 vs 51.3 H2D; concurrent 53.7+49.7 vs 45+40).
@@ -238,12 +239,12 @@ tc_status Pool::span_begin(cudaStream_t s, cudaEvent_t *a) {
     return TC_OK;
 }
 
-tc_status Pool::span_end(cudaStream_t s, int32_t kind, cudaEvent_t a, int64_t bytes) {
+tc_status Pool::span_end(cudaStream_t s, int32_t kind, cudaEvent_t a, int64_t bytes, bool link) {
     if (!timing || !a) return TC_OK;
     cudaEvent_t b = tev_get();
     if (!b) return cuda_fail(cudaErrorMemoryAllocation, "timing event");
     TC_CUDA(cudaEventRecord(b, s), "timing event");
-    spans.push_back(Span{kind, a, b, bytes});
+    spans.push_back(Span{kind, a, b, bytes, link && kind != 2});
     return TC_OK;
 }
 
@@ -255,6 +256,11 @@ void Pool::spans_collect() {
             tacc.ms[sp.kind] += ms;
             tacc.count[sp.kind] += 1;
             tacc.bytes[sp.kind] += sp.bytes;
+            if (sp.link && B > 0) {                             // the host-link side of a transfer
+                const int dir = (sp.kind == 0 || sp.kind == 3) ? 0 : 1;
+                cal_ms[dir] += ms;
+                cal_blocks[dir] += sp.bytes / B;
+            }
             if (timeline.size() < (size_t)timeline_cap) {      // start/end relative to this sync interval's first span
                 float t0 = 0.f;
                 cudaEventElapsedTime(&t0, spans.front().a, sp.a);
@@ -298,8 +304,10 @@ char *Pool::ring_alloc(int64_t bytes, char **dev_ptr) {
 //   DIRECT          A = the single kernel over mapped host memory                 B = -
 //   STAGED gather   A = every piece's gather kernel (aux stream) + an event each  B = the D2H copy per piece (main)
 //   STAGED scatter  A = the H2D copy per piece (main) + an event each             B = the scatter per piece (aux)
-// Pieces of <= pb blocks pipeline the device-side kernels against the copy engine.  If the batch needs more pieces
-// than the staging ring holds (R), phase A does the whole transfer piece by piece (ring reuse waits), B nothing.
+// Pieces pipeline the device-side kernels against the copy engine with few host API calls: an offload is a small
+// head piece (its gather is all that precedes the first D2H byte) then large pieces; an upload is large pieces then
+// a small tail piece (its scatter is all that follows the last H2D byte).  A batch larger than the staging buffer
+// instead runs double-buffered pieces of half the buffer, issued interleaved in phase A (B does nothing).
 tc_status Pool::xfer_init(XferJob &j, bool gather, int32_t mode, const std::vector<XferDesc> *desc,
                           const std::vector<int64_t> *slot_of, cudaStream_t s) {
     j.gather = gather;
@@ -313,16 +321,39 @@ tc_status Pool::xfer_init(XferJob &j, bool gather, int32_t mode, const std::vect
     if (!staging[dir]) TC_CUDA(cudaMalloc(&staging[dir], staging_bytes), "staging alloc");
     j.stg = staging[dir];
     j.sk = gather ? s_off_k : s_up_k;
-    j.pb = std::max<int64_t>(1, std::min<int64_t>({(int64_t)kMaxInlineDesc, piece_bytes / B, staging_bytes / B}));
-    j.R = std::max<int64_t>(1, staging_bytes / (j.pb * B));
-    j.npieces = (j.n + j.pb - 1) / j.pb;
-    j.ring_reuse = j.npieces > j.R;
+    j.cut.clear();
+    const int64_t cap = staging_bytes / B;                       // blocks the staging buffer holds (>= 1)
+    j.ring_reuse = j.n > cap;
+    if (j.ring_reuse) {
+        const int64_t pb = std::max<int64_t>(1, cap / 2);
+        for (int64_t a = 0; a < j.n; a += pb) j.cut.push_back(a);
+    } else {
+        const int64_t edge = std::max<int64_t>(1, head_bytes / B);          // small head (gather) / tail (scatter)
+        const int64_t big = std::max<int64_t>(1, piece_bytes / B);
+        if (gather) {
+            j.cut.push_back(0);
+            for (int64_t a = std::min(edge, j.n); a < j.n; a += big) j.cut.push_back(a);
+        } else {
+            const int64_t body = std::max<int64_t>(0, j.n - edge);
+            for (int64_t a = 0; a < body; a += big) j.cut.push_back(a);
+            j.cut.push_back(body);
+        }
+    }
+    j.cut.push_back(j.n);
+    j.npieces = (int64_t)j.cut.size() - 1;
     j.ev.assign(j.npieces, -1);
     int32_t e0;
     tc_status st = ev_rec(s, &e0);                  // the aux stream starts after the main stream's waits
     if (st != TC_OK) return st;
     TC_CUDA(cudaStreamWaitEvent(j.sk, events[e0], 0), "aux wait");
     return TC_OK;
+}
+
+// Staging address of piece p: contiguous by block index, or one of two halves when double-buffering.
+char *Pool::xfer_base(const XferJob &j, int64_t p) const {
+    if (!j.ring_reuse) return j.stg + j.cut[p] * B;
+    const int64_t pb = j.cut[1] - j.cut[0];
+    return j.stg + (p % 2) * pb * B;
 }
 
 tc_status Pool::ev_rec(cudaStream_t st, int32_t *out) {
@@ -373,21 +404,37 @@ tc_status Pool::xfer_copy(XferJob &j, int64_t a, int64_t b, char *base) {
     return span_end(j.s, to_host ? 3 : 4, t0, (b - a) * B);
 }
 
-// Device-side gather/scatter of pieces [a, b) against the staging slot `base`, descriptors by value.
+// Device-side gather/scatter of pieces [a, b) against the staging slot `base`: descriptors by value in the kernel
+// parameters when they fit, else in the pinned descriptor ring.
 tc_status Pool::xfer_kernel(XferJob &j, int64_t a, int64_t b, char *base) {
-    XferDesc pd[kMaxInlineDesc];
-    for (int64_t i = a; i < b; ++i) {
-        pd[i - a] = (*j.desc)[i];
-        pd[i - a].ext = reinterpret_cast<uint64_t>(base + (i - a) * B);
-    }
     const XferGeom g{N, C, 2 * L};
     cudaEvent_t t0;
-    tc_status s0 = span_begin(j.sk, &t0);
-    if (s0 != TC_OK) return s0;
-    TC_CUDA(launch_xfer_inline(j.gather, pd, (int32_t)(b - a), g, kv, table_dev, ctas[2], nthreads[2], j.sk),
-            j.gather ? "gather kernel" : "scatter kernel");
+    tc_status s0;
+    if (b - a <= kMaxInlineDesc) {
+        XferDesc pd[kMaxInlineDesc];
+        for (int64_t i = a; i < b; ++i) {
+            pd[i - a] = (*j.desc)[i];
+            pd[i - a].ext = reinterpret_cast<uint64_t>(base + (i - a) * B);
+        }
+        if ((s0 = span_begin(j.sk, &t0)) != TC_OK) return s0;
+        TC_CUDA(launch_xfer_inline(j.gather, pd, (int32_t)(b - a), g, kv, table_dev, ctas[2], nthreads[2], j.sk),
+                j.gather ? "gather kernel" : "scatter kernel");
+    } else {
+        char *dptr = nullptr;
+        char *h = ring_alloc((b - a) * (int64_t)sizeof(XferDesc), &dptr);
+        if (!h) return cuda_fail(cudaErrorMemoryAllocation, "descriptor ring");
+        XferDesc *hd = reinterpret_cast<XferDesc *>(h);
+        for (int64_t i = a; i < b; ++i) {
+            hd[i - a] = (*j.desc)[i];
+            hd[i - a].ext = reinterpret_cast<uint64_t>(base + (i - a) * B);
+        }
+        if ((s0 = span_begin(j.sk, &t0)) != TC_OK) return s0;
+        TC_CUDA(launch_xfer(j.gather, reinterpret_cast<const XferDesc *>(dptr), b - a, g, kv, table_dev, ctas[2],
+                            nthreads[2], variant[2], j.sk),
+                j.gather ? "gather kernel" : "scatter kernel");
+    }
     ++n_launch;
-    return span_end(j.sk, j.gather ? 0 : 1, t0, (b - a) * B);
+    return span_end(j.sk, j.gather ? 0 : 1, t0, (b - a) * B, /*link=*/false);
 }
 
 tc_status Pool::xfer_phase_a(XferJob &j) {
@@ -415,19 +462,19 @@ tc_status Pool::xfer_phase_a(XferJob &j) {
     }
     std::vector<int32_t> done(j.ring_reuse ? j.npieces : 0, -1);
     for (int64_t p = 0; p < j.npieces; ++p) {
-        const int64_t a = p * j.pb, b = std::min(j.n, a + j.pb);
-        char *base = j.stg + (p % j.R) * j.pb * B;
+        const int64_t a = j.cut[p], b = j.cut[p + 1];
+        char *base = xfer_base(j, p);
         if (j.gather) {
-            if (j.ring_reuse && p >= j.R) TC_CUDA(cudaStreamWaitEvent(j.sk, events[done[p - j.R]], 0), "ring reuse");
+            if (j.ring_reuse && p >= 2) TC_CUDA(cudaStreamWaitEvent(j.sk, events[done[p - 2]], 0), "ring reuse");
             if ((st = xfer_kernel(j, a, b, base)) != TC_OK) return st;
             if ((st = ev_rec(j.sk, &j.ev[p])) != TC_OK) return st;
-            if (j.ring_reuse) {                        // interleaved: copy now, mark the ring slot free after it
+            if (j.ring_reuse) {                        // interleaved: copy now, mark the half free after it
                 TC_CUDA(cudaStreamWaitEvent(j.s, events[j.ev[p]], 0), "gather->D2H wait");
                 if ((st = xfer_copy(j, a, b, base)) != TC_OK) return st;
                 if ((st = ev_rec(j.s, &done[p])) != TC_OK) return st;
             }
         } else {
-            if (j.ring_reuse && p >= j.R) TC_CUDA(cudaStreamWaitEvent(j.s, events[done[p - j.R]], 0), "ring reuse");
+            if (j.ring_reuse && p >= 2) TC_CUDA(cudaStreamWaitEvent(j.s, events[done[p - 2]], 0), "ring reuse");
             if ((st = xfer_copy(j, a, b, base)) != TC_OK) return st;
             if ((st = ev_rec(j.s, &j.ev[p])) != TC_OK) return st;
             if (j.ring_reuse) {
@@ -444,10 +491,9 @@ tc_status Pool::xfer_phase_a(XferJob &j) {
 tc_status Pool::xfer_phase_b(XferJob &j) {
     if (j.n == 0 || j.mode != TC_XFER_STAGED || j.ring_reuse) return TC_OK;
     tc_status st;
-    int32_t last = -1;
     for (int64_t p = 0; p < j.npieces; ++p) {
-        const int64_t a = p * j.pb, b = std::min(j.n, a + j.pb);
-        char *base = j.stg + (p % j.R) * j.pb * B;
+        const int64_t a = j.cut[p], b = j.cut[p + 1];
+        char *base = xfer_base(j, p);
         if (j.gather) {
             TC_CUDA(cudaStreamWaitEvent(j.s, events[j.ev[p]], 0), "gather->D2H wait");
             if ((st = xfer_copy(j, a, b, base)) != TC_OK) return st;
@@ -457,6 +503,7 @@ tc_status Pool::xfer_phase_b(XferJob &j) {
         }
     }
     if (!j.gather) {                                   // the upload completes when its last scatter has
+        int32_t last;
         if ((st = ev_rec(j.sk, &last)) != TC_OK) return st;
         TC_CUDA(cudaStreamWaitEvent(j.s, events[last], 0), "scatter->upload join");
     }

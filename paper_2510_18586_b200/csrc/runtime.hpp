@@ -87,7 +87,8 @@ struct Pool {
     // streams / events
     cudaStream_t s_up = nullptr, s_off = nullptr, s_compute = nullptr;
     cudaStream_t s_up_k = nullptr, s_off_k = nullptr;   // staged mode: device-side kernels of each direction
-    int64_t piece_bytes = 32ll << 20;                   // staged pipeline granularity
+    int64_t piece_bytes = 256ll << 20;                  // staged pipeline: large pieces
+    int64_t head_bytes = 4ll << 20;                     // ... and the small head (offload) / tail (upload) piece
     bool use_batch_memcpy = true;
     cudaEvent_t ev_compute = nullptr;
     std::vector<cudaStream_t> foreign;       // caller streams used by the device tier
@@ -119,6 +120,7 @@ struct Pool {
         int32_t kind;
         cudaEvent_t a, b;
         int64_t bytes;
+        bool link;                           // host-link side of a transfer (DMA or direct kernel)
     };
     bool timing = false;
     std::vector<Span> spans;
@@ -126,11 +128,13 @@ struct Pool {
     tc_timing_t tacc{};
     cudaEvent_t tev_get();
     tc_status span_begin(cudaStream_t s, cudaEvent_t *a);
-    tc_status span_end(cudaStream_t s, int32_t kind, cudaEvent_t a, int64_t bytes);
+    tc_status span_end(cudaStream_t s, int32_t kind, cudaEvent_t a, int64_t bytes, bool link = true);
     void spans_collect();
     std::vector<tc_span_t> timeline;         // per-span records (tc_timeline), capped
     int64_t timeline_cap = 0;
     int64_t sync_count = 0;
+    double cal_ms[2] = {0, 0};               // link-side transfer time per direction (tc_xfer_model_measure)
+    int64_t cal_blocks[2] = {0, 0};
 
     // counters / errors
     int64_t n_launch = 0, n_memcpy = 0, bytes_d2h = 0, bytes_h2d = 0;
@@ -197,10 +201,12 @@ struct Pool {
         const std::vector<XferDesc> *desc = nullptr;
         const std::vector<int64_t> *slot_of = nullptr;
         cudaStream_t s = nullptr, sk = nullptr;
-        int64_t n = 0, pb = 1, R = 1, npieces = 0;
+        int64_t n = 0, npieces = 0;
+        std::vector<int64_t> cut;            // piece p = blocks [cut[p], cut[p+1])
         char *stg = nullptr;
         std::vector<int32_t> ev;
     };
+    char *xfer_base(const XferJob &j, int64_t p) const;
     tc_status xfer_init(XferJob &j, bool gather, int32_t mode, const std::vector<XferDesc> *desc,
                         const std::vector<int64_t> *slot_of, cudaStream_t s);
     tc_status xfer_phase_a(XferJob &j);

@@ -1,0 +1,143 @@
+"""ctypes binding of the decision layers around the hot path (include/tokencake.h NEXT-3 / NEXT-4 sections).
+
+Marshalling only; the arithmetic runs in libtokencake.so (csrc/sched.cpp).
+  NEXT-3 Time Scheduler: Eq. 1 forecast + EWMA, transfer-cost model (calibrated from a pool's measured transfers),
+         Alg. 1 ShouldOffload, predictive-upload plan.
+  NEXT-4 Space Scheduler: static / dynamic priority, critical selection, Alg. 2 reservations, applied to a pool.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import TcError, _ptr, lib
+
+D, I32, I64, P = ctypes.c_double, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p
+
+
+class FcStat(ctypes.Structure):
+    _fields_ = [("t_hist", D), ("n_obs", I64), ("cold_start", D)]
+
+
+class XferModel(ctypes.Structure):
+    _fields_ = [("offload_ms_per_block", D), ("upload_ms_per_block", D), ("fixed_ms", D)]
+
+
+class OffloadDecision(ctypes.Structure):
+    _fields_ = [("offload", I32), ("match", I32), ("t_transfer", D), ("t_window", D), ("n_capacity", D)]
+
+
+class UploadPlan(ctypes.Structure):
+    _fields_ = [("immediate", I32), ("upload_start", D), ("reservation_deadline", D), ("predicted_finish", D)]
+
+
+class PartitionParams(ctypes.Structure):
+    _fields_ = [("gpu_usage_high", D), ("gpu_usage_low", D), ("adjustment_step", D), ("reserve_ratio_max", D)]
+
+
+_SIG = {
+    "tc_fc_predict": (D, [ctypes.POINTER(FcStat), D, D]),
+    "tc_fc_observe": (I32, [ctypes.POINTER(FcStat), D, D]),
+    "tc_transfer_ms": (D, [ctypes.POINTER(XferModel), I64]),
+    "tc_xfer_model_measure": (I32, [P, ctypes.POINTER(XferModel)]),
+    "tc_should_offload": (I32, [I64, D, D, D, ctypes.POINTER(D), I64, ctypes.POINTER(OffloadDecision)]),
+    "tc_plan_upload": (I32, [D, D, D, D, D, ctypes.POINTER(UploadPlan)]),
+    "tc_static_priority": (D, [D, I32, I32]),
+    "tc_dynamic_priority": (D, [D, D]),
+    "tc_select_critical": (I32, [I32, ctypes.POINTER(D), D, ctypes.POINTER(ctypes.c_uint8)]),
+    "tc_update_reservations": (I32, [ctypes.POINTER(PartitionParams), ctypes.POINTER(D), I64, I64, I32,
+                                     ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(D), ctypes.POINTER(I64),
+                                     ctypes.POINTER(D), ctypes.POINTER(I64)]),
+    "tc_apply_reservations": (I32, [P, I32, ctypes.POINTER(I32), ctypes.POINTER(I64)]),
+}
+for _n, (_r, _a) in _SIG.items():
+    _f = getattr(lib, _n)
+    _f.restype, _f.argtypes = _r, _a
+
+
+def _check(st):
+    if st != 0:
+        raise TcError(st, lib.tc_strerror(st).decode())
+
+
+# ------------------------------------------------------------------------------------------------ NEXT-3
+def fc_predict(t_hist, n_obs, cold_start, t_req=None, alpha=0.5) -> float:
+    s = FcStat(0.0 if t_hist is None else t_hist, n_obs, cold_start)
+    return lib.tc_fc_predict(ctypes.byref(s), -1.0 if t_req is None else float(t_req), alpha)
+
+
+def fc_observe(t_hist, n_obs, observed, beta=0.5) -> tuple:
+    s = FcStat(0.0 if t_hist is None else t_hist, n_obs, 0.0)
+    _check(lib.tc_fc_observe(ctypes.byref(s), observed, beta))
+    return s.t_hist, s.n_obs
+
+
+def transfer_ms(n_blocks, offload_ms_per_block, upload_ms_per_block, fixed_ms=0.0) -> float:
+    m = XferModel(offload_ms_per_block, upload_ms_per_block, fixed_ms)
+    return lib.tc_transfer_ms(ctypes.byref(m), n_blocks)
+
+
+def xfer_model_measure(pool) -> dict:
+    m = XferModel()
+    _check(lib.tc_xfer_model_measure(pool._h, ctypes.byref(m)))
+    return {"offload_ms_per_block": m.offload_ms_per_block, "upload_ms_per_block": m.upload_ms_per_block,
+            "fixed_ms": m.fixed_ms}
+
+
+def should_offload(n_blocks, t_fc, t_transfer, v_tok_s, waiting_tokens) -> dict:
+    w = np.ascontiguousarray(np.asarray(waiting_tokens, dtype=np.float64).reshape(-1))
+    out = OffloadDecision()
+    _check(lib.tc_should_offload(n_blocks, t_fc, t_transfer, v_tok_s, _ptr(w, D) if w.size else None, w.size,
+                                 ctypes.byref(out)))
+    return {"offload": bool(out.offload), "match": out.match, "t_transfer": out.t_transfer,
+            "t_window": out.t_window, "n_capacity": out.n_capacity}
+
+
+def plan_upload(call_start, t_final, upload_ms, offload_ms, lead_ms=100.0) -> dict:
+    out = UploadPlan()
+    _check(lib.tc_plan_upload(call_start, t_final, upload_ms, offload_ms, lead_ms, ctypes.byref(out)))
+    return {"immediate": bool(out.immediate), "upload_start": out.upload_start,
+            "reservation_deadline": out.reservation_deadline, "predicted_finish": out.predicted_finish}
+
+
+# ------------------------------------------------------------------------------------------------ NEXT-4
+def static_priority(w, depth, out_degree) -> float:
+    return lib.tc_static_priority(w, depth, out_degree)
+
+
+def dynamic_priority(time_wait_ms, tokens_req) -> float:
+    return lib.tc_dynamic_priority(time_wait_ms, tokens_req)
+
+
+def select_critical(scores: dict, ratio: float) -> list:
+    """scores keyed by type name; the library breaks ties by index, so names are passed in sorted order."""
+    names = sorted(scores)
+    sc = np.asarray([scores[n] for n in names], dtype=np.float64)
+    crit = np.zeros(max(len(names), 1), dtype=np.uint8)
+    _check(lib.tc_select_critical(len(names), _ptr(sc, D) if len(names) else None, ratio,
+                                  _ptr(crit, ctypes.c_uint8)))
+    return [n for n, c in zip(names, crit) if c]
+
+
+def update_reservations(total_reserve_ratio, usage, tot_blks, critical, scores, type_usage,
+                        gpu_usage_high=0.85, gpu_usage_low=0.50, adjustment_step=0.05, reserve_ratio_max=0.40):
+    names = sorted(scores) if scores else sorted(critical)
+    crit = np.asarray([1 if n in critical else 0 for n in names], dtype=np.uint8)
+    sc = np.asarray([scores.get(n, 0.0) for n in names], dtype=np.float64)
+    tu = np.asarray([type_usage.get(n, 0) for n in names], dtype=np.int64)
+    res = np.zeros(max(len(names), 1), dtype=np.int64)
+    pp = PartitionParams(gpu_usage_high, gpu_usage_low, adjustment_step, reserve_ratio_max)
+    r = ctypes.c_double(total_reserve_ratio)
+    R = ctypes.c_double()
+    k = len(names)
+    _check(lib.tc_update_reservations(ctypes.byref(pp), ctypes.byref(r), usage, tot_blks, k,
+                                      _ptr(crit, ctypes.c_uint8) if k else None, _ptr(sc, D) if k else None,
+                                      _ptr(tu, I64) if k else None, ctypes.byref(R), _ptr(res, I64) if k else None))
+    return r.value, R.value, {n: int(v) for n, v, c in zip(names, res, crit) if c}
+
+
+def apply_reservations(pool, quotas: dict):
+    cls = np.asarray(list(quotas.keys()), dtype=np.int32)
+    num = np.asarray(list(quotas.values()), dtype=np.int64)
+    _check(lib.tc_apply_reservations(pool._h, len(cls), _ptr(cls, I32), _ptr(num, I64)))

@@ -208,3 +208,15 @@ def test_full_size_config_parity(name, world):
     others = rng.choice(cfg.N, size=512, replace=False)
     sample_check(c, cfg, o.store.prov, others, cfg.seed, rank, world, rng)
     c.close()
+
+
+@pytest.mark.parametrize("head_kib,piece_kib", [(1, 2), (3, 1024), (64, 64)])
+def test_staged_piece_plans_bytes(monkeypatch, head_kib, piece_kib):
+    """Staged pipelining with several pieces per batch: small head/tail pieces, multi-block pieces, and pieces above
+    the inline-descriptor limit (descriptors from the pinned ring); B = 1 KiB blocks."""
+    monkeypatch.setenv("TC_HEAD_KIB", str(head_kib))
+    monkeypatch.setenv("TC_PIECE_KIB", str(piece_kib))
+    L, H, D, T, N, S = 1, 1, 64, 4, 600, 400
+    for seed in range(3):
+        ops = fuzz_script(seed + 77, n_ops=60, n_agents=3, n_classes=2, N=N, max_alloc=150)
+        run_script(ops, L, H, D, N, S, "staged", ncls=2, seed=seed + 3, T=T)
