@@ -201,6 +201,8 @@ def run_ours(args):
                 ooff = np.zeros(len(tabs) + 1, dtype=np.int64)
                 ooff[1:] = np.cumsum([len(t) for t in tabs])
                 ids = np.ascontiguousarray(np.concatenate(tabs)) if tabs else np.zeros(1, np.int32)
+                if record is not None:
+                    record("start")
                 _, out_h = pool.cycle_arrays(hs, uoff, ags, ooff, ids)
                 for a, h, t in zip(ags, out_h, tabs):
                     handles[int(a)] = int(h)
@@ -238,12 +240,11 @@ def run_ours(args):
         ev = {}
 
         def record(tag):
-            if tag == "end":
-                for nm, st in (("up1", ups), ("off1", offs_)):
-                    e = torch.cuda.Event(enable_timing=True); e.record(st); ev[nm] = e
-        for nm, st in (("up0", ups), ("off0", offs_)):
-            e = torch.cuda.Event(enable_timing=True); e.record(st); ev[nm] = e
-        t0 = time.perf_counter()
+            # device clock: from just before the tc_cycle call to the end of both copy streams' work
+            pair = (("up0", ups), ("off0", offs_)) if tag == "start" else (("up1", ups), ("off1", offs_))
+            for nm, st in pair:
+                e = torch.cuda.Event(enable_timing=True); e.record(st); ev[nm] = e
+        t0 = time.perf_counter()                # host clock (e2e): the whole public-API cycle incl. id lookups
         nu, no = cycle(record)
         t1 = time.perf_counter()
         ref = ev["up0"]
@@ -382,6 +383,13 @@ def timeline_summary(spans):
         v = [d[k] for d in by.values() if k in d]
         out[k] = {"first_start_ms": statistics.mean(x[0] for x in v), "last_end_ms": statistics.mean(x[1] for x in v)}
     out["step_span_ms"] = statistics.mean(max(x[1] for x in d.values()) for d in by.values())
+    # per step: how late each DMA direction starts, and how long the step runs past its last DMA byte
+    dma = [d for d in by.values() if "memcpy_d2h" in d and "memcpy_h2d" in d]
+    if dma:
+        out["d2h_start_ms"] = statistics.mean(d["memcpy_d2h"][0] for d in dma)
+        out["h2d_start_ms"] = statistics.mean(d["memcpy_h2d"][0] for d in dma)
+        out["tail_after_last_dma_ms"] = statistics.mean(
+            max(x[1] for x in d.values()) - max(d["memcpy_d2h"][1], d["memcpy_h2d"][1]) for d in dma)
     out["steps"] = len(by)
     return out
 

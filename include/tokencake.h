@@ -78,6 +78,9 @@ typedef struct tc_pool_desc {
     int32_t xfer_d2h, xfer_h2d;  /* tc_xfer_mode per direction */
     int64_t staging_bytes;       /* device staging ring per direction for STAGED mode; 0 -> 256 MiB */
     int64_t desc_bytes;          /* pinned descriptor ring; 0 -> 16 MiB */
+    int32_t unbuffered;          /* ABLATION ONLY (Fig. 11): no CPU block buffer — each offload
+                                    cudaHostAlloc's its own pinned memory, freed (cudaFreeHost) when its upload
+                                    retires; the bursty host allocation pattern of P:470-479.  0 = normal. */
 } tc_pool_desc;
 
 typedef struct tc_stats_t {

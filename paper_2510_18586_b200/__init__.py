@@ -53,7 +53,7 @@ class PoolDesc(ctypes.Structure):
         ("host_slots", ctypes.c_int64), ("n_classes", ctypes.c_int32), ("max_agents", ctypes.c_int32),
         ("max_blocks_per_agent", ctypes.c_int32), ("kv_dev", ctypes.c_void_p), ("table_dev", ctypes.c_void_p),
         ("xfer_d2h", ctypes.c_int32), ("xfer_h2d", ctypes.c_int32), ("staging_bytes", ctypes.c_int64),
-        ("desc_bytes", ctypes.c_int64),
+        ("desc_bytes", ctypes.c_int64), ("unbuffered", ctypes.c_int32),
     ]
 
 
@@ -157,7 +157,7 @@ class Pool:
                  n_blocks: int = 64, *, device: int = 0, shard_rank: int = 0, shard_world: int = 1,
                  host_slots: int = 0, n_classes: int = 8, max_agents: int = 1024, max_blocks_per_agent: int = 4096,
                  xfer_d2h: int = XFER_AUTO, xfer_h2d: int = XFER_AUTO, staging_bytes: int = 0,
-                 torch_memory: bool = True):
+                 torch_memory: bool = True, unbuffered: bool = False):
         d = PoolDesc()
         lib.tc_pool_desc_init(ctypes.byref(d), layers, kv_heads, head_dim, block_tokens, DTYPES[dtype], n_blocks)
         d.device = device
@@ -166,6 +166,7 @@ class Pool:
         d.n_classes, d.max_agents, d.max_blocks_per_agent = n_classes, max_agents, max_blocks_per_agent
         d.xfer_d2h, d.xfer_h2d = xfer_d2h, xfer_h2d
         d.staging_bytes = staging_bytes
+        d.unbuffered = 1 if unbuffered else 0
         self._keep = []
         self.device = device
         self.meta_only = device < 0

@@ -274,7 +274,7 @@ tc_status tc_handle_host(tc_pool *p, tc_handle h, int64_t i, const void **host_p
         auto it = P.handles.find(h);
         if (it == P.handles.end() || it->second.state != tc::kOffloaded) return TC_E_HANDLE;
         if (i < 0 || i >= (int64_t)it->second.slots.size() || !host_ptr) return TC_E_INVAL;
-        *host_ptr = P.slots.host + it->second.slots[i] * P.B;
+        *host_ptr = P.host_ptr(it->second.slots[i]);
         return TC_OK;
     }
     TC_CATCH

@@ -105,6 +105,8 @@ Pool::~Pool() {
     for (auto st : staging)
         if (st) cudaFree(st);
     if (slots.host) cudaFreeHost(slots.host);
+    for (auto &kv_ : extra)
+        if (kv_.second.host) cudaFreeHost(kv_.second.host);
     if (ring_host) cudaFreeHost(ring_host);
 }
 
@@ -136,6 +138,8 @@ tc_status Pool::create(const tc_pool_desc &d) {
     for (int64_t i = 0; i < S; ++i) slots.free_list[i] = S - 1 - i;   // pop() yields 0, 1, 2, ...
     device = d.device;
     meta_only = d.device < 0;
+    unbuffered = d.unbuffered != 0;
+    next_slot = S;
     mode_d2h = d.xfer_d2h;
     mode_h2d = d.xfer_h2d;
     if (mode_d2h < 0 || mode_d2h > 2 || mode_h2d < 0 || mode_h2d > 2) return TC_E_INVAL;
@@ -273,6 +277,18 @@ void Pool::spans_collect() {
     spans.clear();
 }
 
+char *Pool::host_ptr(int64_t slot) const {
+    if (slot < slots.count) return slots.host + slot * B;
+    auto sl = std::prev(extra.upper_bound(slot));
+    return sl->second.host + (slot - sl->first) * B;
+}
+
+char *Pool::host_dev_ptr(int64_t slot) const {
+    if (slot < slots.count) return slots.dev + slot * B;
+    auto sl = std::prev(extra.upper_bound(slot));
+    return sl->second.dev + (slot - sl->first) * B;
+}
+
 // Pinned, mapped scratch for descriptors and table pushes.  Wrapping waits for every stream that may still read it.
 char *Pool::ring_alloc(int64_t bytes, char **dev_ptr) {
     bytes = (bytes + 255) & ~255ll;
@@ -302,7 +318,7 @@ char *Pool::ring_alloc(int64_t bytes, char **dev_ptr) {
 // A transfer of desc.size() blocks, enqueued in two phases so that one scheduling cycle can interleave its two
 // directions on the host (tc_cycle) and both links start as early as possible:
 //   DIRECT          A = the single kernel over mapped host memory                 B = -
-//   STAGED gather   A = every piece's gather kernel (aux stream) + an event each  B = the D2H copy per piece (main)
+//   STAGED gather   A = per piece: gather kernel (aux stream), event, D2H copy (main)   B = -
 //   STAGED scatter  A = the H2D copy per piece (main) + an event each             B = the scatter per piece (aux)
 // Pieces pipeline the device-side kernels against the copy engine with few host API calls: an offload is a small
 // head piece (its gather is all that precedes the first D2H byte) then large pieces; an upload is large pieces then
@@ -373,8 +389,8 @@ tc_status Pool::xfer_copy(XferJob &j, int64_t a, int64_t b, char *base) {
     cp_dst.clear(); cp_src.clear(); cp_size.clear();
     for (int64_t i = a; i < b;) {
         int64_t k = i + 1;
-        while (k < b && slot_of[k] == slot_of[k - 1] + 1) ++k;      // contiguous run of host slots
-        char *hp = slots.host + slot_of[i] * B;
+        char *hp = host_ptr(slot_of[i]);
+        while (k < b && host_ptr(slot_of[k]) == hp + (k - i) * B) ++k;   // contiguous run of host memory
         char *dp = base + (i - a) * B;
         cp_dst.push_back(to_host ? (void *)hp : (void *)dp);
         cp_src.push_back(to_host ? (void *)dp : (void *)hp);
@@ -450,7 +466,7 @@ tc_status Pool::xfer_phase_a(XferJob &j) {
         XferDesc *hd = reinterpret_cast<XferDesc *>(h);
         for (int64_t i = 0; i < j.n; ++i) {
             hd[i] = (*j.desc)[i];
-            if (!dev_tier) hd[i].ext = reinterpret_cast<uint64_t>(slots.dev + (*j.slot_of)[i] * B);
+            if (!dev_tier) hd[i].ext = reinterpret_cast<uint64_t>(host_dev_ptr((*j.slot_of)[i]));
         }
         cudaEvent_t t0;
         if ((st = span_begin(j.s, &t0)) != TC_OK) return st;
@@ -468,11 +484,11 @@ tc_status Pool::xfer_phase_a(XferJob &j) {
             if (j.ring_reuse && p >= 2) TC_CUDA(cudaStreamWaitEvent(j.sk, events[done[p - 2]], 0), "ring reuse");
             if ((st = xfer_kernel(j, a, b, base)) != TC_OK) return st;
             if ((st = ev_rec(j.sk, &j.ev[p])) != TC_OK) return st;
-            if (j.ring_reuse) {                        // interleaved: copy now, mark the half free after it
-                TC_CUDA(cudaStreamWaitEvent(j.s, events[j.ev[p]], 0), "gather->D2H wait");
-                if ((st = xfer_copy(j, a, b, base)) != TC_OK) return st;
-                if ((st = ev_rec(j.s, &done[p])) != TC_OK) return st;
-            }
+            // the D2H copy of a piece is issued right after its gather, so the link starts after the small
+            // head piece's gather and a handful of API calls
+            TC_CUDA(cudaStreamWaitEvent(j.s, events[j.ev[p]], 0), "gather->D2H wait");
+            if ((st = xfer_copy(j, a, b, base)) != TC_OK) return st;
+            if (j.ring_reuse && (st = ev_rec(j.s, &done[p])) != TC_OK) return st;
         } else {
             if (j.ring_reuse && p >= 2) TC_CUDA(cudaStreamWaitEvent(j.s, events[done[p - 2]], 0), "ring reuse");
             if ((st = xfer_copy(j, a, b, base)) != TC_OK) return st;
@@ -489,7 +505,7 @@ tc_status Pool::xfer_phase_a(XferJob &j) {
 }
 
 tc_status Pool::xfer_phase_b(XferJob &j) {
-    if (j.n == 0 || j.mode != TC_XFER_STAGED || j.ring_reuse) return TC_OK;
+    if (j.n == 0 || j.mode != TC_XFER_STAGED || j.ring_reuse || j.gather) return TC_OK;
     tc_status st;
     for (int64_t p = 0; p < j.npieces; ++p) {
         const int64_t a = j.cut[p], b = j.cut[p + 1];
@@ -606,14 +622,32 @@ tc_status Pool::plan_offload(OffPlan &P, int32_t na, const int32_t *ags, const i
                 return TC_E_INVAL;
             stamp[b] = epoch;
         }
-        if ((int64_t)slots.free_list.size() < off[k + 1]) return TC_E_NOHOST;   // refuse, no change
+        if (!unbuffered && (int64_t)slots.free_list.size() < off[k + 1]) return TC_E_NOHOST;   // refuse
     }
     P.na = na; P.ags = ags; P.off = off; P.ids = ids;
     const int64_t n = off[na];
     P.desc.resize(n);
     P.slot_of.resize(n);
-    const size_t top = slots.free_list.size();
-    for (int64_t i = 0; i < n; ++i) P.slot_of[i] = slots.free_list[top - 1 - i];   // LIFO pop order (A16)
+    if (unbuffered) {
+        // Fig. 11 ablation: no CPU block buffer — pinned host memory is allocated for this offload now and freed
+        // when its upload retires (the bursty OS allocation pattern of P:470-479).
+        char *h = nullptr;
+        if (meta_only) {
+            h = nullptr;
+        } else if (cudaHostAlloc(reinterpret_cast<void **>(&h), (size_t)(n * B),
+                                 cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
+            cudaGetLastError();
+            return TC_E_NOHOST;
+        }
+        char *dh = nullptr;
+        if (h) cudaHostGetDevicePointer(reinterpret_cast<void **>(&dh), h, 0);
+        extra[next_slot] = ExtraSlab{h, dh, n, n};
+        for (int64_t i = 0; i < n; ++i) P.slot_of[i] = next_slot + i;
+        next_slot += n;
+    } else {
+        const size_t top = slots.free_list.size();
+        for (int64_t i = 0; i < n; ++i) P.slot_of[i] = slots.free_list[top - 1 - i];   // LIFO pop order (A16)
+    }
     for (int32_t k = 0; k < na; ++k)
         for (int64_t i = off[k]; i < off[k + 1]; ++i)
             P.desc[i] = XferDesc{ids[i], ags[k] * max_bpa + alloc.own_pos[ids[i]], 0};
@@ -637,7 +671,7 @@ tc_status Pool::offload_waits(const OffPlan &P) {
 // commit (a3 logical effects + a4 pending free); ev = the offload's completion event
 void Pool::commit_offload(const OffPlan &P, int32_t ev, tc_handle *out) {
     const int64_t n = P.off[P.na];
-    slots.free_list.resize(slots.free_list.size() - n);
+    if (!unbuffered) slots.free_list.resize(slots.free_list.size() - n);
     for (int32_t k = 0; k < P.na; ++k) {
         const int32_t a = P.ags[k];
         AgentRec &ag = agents[a];
@@ -932,7 +966,17 @@ tc_status Pool::sync() {
     }
     pending_dev.clear();
     // released host slots back to the buffer; pushed in reverse so later pops replay ascending runs
-    for (auto it = slots.released.rbegin(); it != slots.released.rend(); ++it) slots.free_list.push_back(*it);
+    for (auto it = slots.released.rbegin(); it != slots.released.rend(); ++it) {
+        if (*it < slots.count) {
+            slots.free_list.push_back(*it);
+            continue;
+        }
+        auto sl = std::prev(extra.upper_bound(*it));      // unbuffered ablation: free the slab with its last block
+        if (--sl->second.live == 0) {
+            if (sl->second.host) cudaFreeHost(sl->second.host);
+            extra.erase(sl);
+        }
+    }
     slots.released.clear();
     for (auto it = handles.begin(); it != handles.end();) {
         if (it->second.state == kUploaded) {

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <set>
 #include <string>
 #include <unordered_map>
@@ -207,6 +208,17 @@ struct Pool {
         std::vector<int32_t> ev;
     };
     char *xfer_base(const XferJob &j, int64_t p) const;
+    // host address (and its device mapping) of a host slot id: the CPU block buffer, or an ablation slab
+    char *host_ptr(int64_t slot) const;
+    char *host_dev_ptr(int64_t slot) const;
+    // Fig. 11 ablation (tc_pool_desc.unbuffered): per-offload pinned slabs instead of the CPU block buffer
+    struct ExtraSlab {
+        char *host, *dev;
+        int64_t n, live;
+    };
+    bool unbuffered = false;
+    std::map<int64_t, ExtraSlab> extra;      // first slot id -> slab
+    int64_t next_slot = 0;
     tc_status xfer_init(XferJob &j, bool gather, int32_t mode, const std::vector<XferDesc> *desc,
                         const std::vector<int64_t> *slot_of, cudaStream_t s);
     tc_status xfer_phase_a(XferJob &j);

@@ -220,3 +220,19 @@ def test_staged_piece_plans_bytes(monkeypatch, head_kib, piece_kib):
     for seed in range(3):
         ops = fuzz_script(seed + 77, n_ops=60, n_agents=3, n_classes=2, N=N, max_alloc=150)
         run_script(ops, L, H, D, N, S, "staged", ncls=2, seed=seed + 3, T=T)
+
+
+def test_unbuffered_ablation_bytes():
+    """The Fig. 11 ablation mode (per-offload cudaHostAlloc, no CPU block buffer) moves the same bytes."""
+    L, H, D, N, S = 2, 2, 64, 48, 4
+    pool0 = content.pool_bytes(4, L, N, 16, H, D)
+    o = OraclePool(N, 64, n_classes=2, store=BytesStore(pool0, 64))
+    c = tcb.Pool(L, H, D, 16, "bf16", N, device=0, host_slots=S, n_classes=2, unbuffered=True)
+    c.fill(4)
+    ops = fuzz_script(5, n_ops=80, n_agents=3, n_classes=2, N=N)
+    ro, rc = Replayer(o), Replayer(c)
+    for i, op in enumerate(ops):
+        a, b = ro.step(op), rc.step(op)
+        assert a == b, (i, op, a, b)
+    c.sync()
+    assert np.array_equal(c.kv_tensor().cpu().numpy(), o.store.pool)
