@@ -195,6 +195,11 @@ typedef struct tc_timing_t {
     double ms[5];
     int64_t count[5];
     int64_t bytes[5];
+    /* device-side kernel durations (first CTA start -> last CTA end on %globaltimer, no host launch latency):
+       0 offload (gather) kernels, 1 upload (scatter) kernels, 2 device-tier kernels */
+    double kernel_ms[3];
+    int64_t kernel_count[3];
+    int64_t kernel_bytes[3];
 } tc_timing_t;
 /* enable != 0 turns span recording on (off by default: zero overhead).  If out != NULL it receives the totals
    accumulated since the previous call, which are then reset. */

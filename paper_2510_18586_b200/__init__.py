@@ -58,7 +58,9 @@ class PoolDesc(ctypes.Structure):
 
 
 class Timing(ctypes.Structure):
-    _fields_ = [("ms", ctypes.c_double * 5), ("count", ctypes.c_int64 * 5), ("bytes", ctypes.c_int64 * 5)]
+    _fields_ = [("ms", ctypes.c_double * 5), ("count", ctypes.c_int64 * 5), ("bytes", ctypes.c_int64 * 5),
+                ("kernel_ms", ctypes.c_double * 3), ("kernel_count", ctypes.c_int64 * 3),
+                ("kernel_bytes", ctypes.c_int64 * 3)]
 
 
 class Span(ctypes.Structure):
@@ -367,10 +369,14 @@ class Pool:
         return d
 
     def timing(self, enable: bool = True) -> dict:
-        """Enable/disable per-launch event timing; returns {kind: (ms, count, bytes)} accumulated since last call."""
+        """Enable/disable per-launch timing; returns {kind: (ms, count, bytes)} accumulated since the last call:
+        event spans per kind (TIMING_KINDS) plus device-side kernel durations under 'dev_<kind>'."""
         t = Timing()
         self._check(lib.tc_timing(self._h, 1 if enable else 0, ctypes.byref(t)))
-        return {k: (t.ms[i], t.count[i], t.bytes[i]) for i, k in enumerate(TIMING_KINDS)}
+        out = {k: (t.ms[i], t.count[i], t.bytes[i]) for i, k in enumerate(TIMING_KINDS)}
+        for i, k in enumerate(TIMING_KINDS[:3]):
+            out["dev_" + k] = (t.kernel_ms[i], t.kernel_count[i], t.kernel_bytes[i])
+        return out
 
     def timeline_arm(self, cap: int = 100000):
         n = ctypes.c_int64()

@@ -40,6 +40,20 @@ __device__ __forceinline__ void warp_copy(int4 *__restrict__ dst, const int4 *__
     for (; v < nv; v += 32) st_stream(dst + v, ld_stream(src + v));
 }
 
+// Device-side launch timing (tc_timing): earliest CTA start / latest CTA end on the %globaltimer clock (ns), so a
+// kernel's duration excludes host launch latency.  g.ts = {start, end}, pre-set to {UINT64_MAX, 0}; null = off.
+__device__ __forceinline__ unsigned long long now_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void ts_begin(const XferGeom &g) {
+    if (g.ts) atomicMin(g.ts, now_ns());
+}
+__device__ __forceinline__ void ts_end(const XferGeom &g) {
+    if (g.ts) atomicMax(g.ts + 1, now_ns());
+}
+
 template <bool kGather>
 __device__ __forceinline__ void xfer_body(const XferDesc *__restrict__ desc, int64_t n, const XferGeom &g,
                                           char *__restrict__ kv, int32_t *__restrict__ table, int64_t chunks_per_cta,
@@ -47,6 +61,7 @@ __device__ __forceinline__ void xfer_body(const XferDesc *__restrict__ desc, int
     const int64_t M = n * g.two_l;
     const int64_t j0 = (int64_t)blockIdx.x * chunks_per_cta;
     if (j0 >= M) return;
+    if (threadIdx.x == 0) ts_begin(g);
     const int64_t j1 = min(M, j0 + chunks_per_cta);
     const int64_t i0 = j0 / g.two_l;
     const int nb = (int)((j1 - 1) / g.two_l - i0 + 1);
@@ -71,6 +86,10 @@ __device__ __forceinline__ void xfer_body(const XferDesc *__restrict__ desc, int
         else
             warp_copy(reinterpret_cast<int4 *>(pool_chunk), reinterpret_cast<const int4 *>(ext_chunk), nv, lane);
         if (lk == 0 && lane == 0 && d.tab >= 0) table[d.tab] = kGather ? -1 : d.blk;
+    }
+    if (g.ts) {
+        __syncthreads();
+        if (threadIdx.x == 0) ts_end(g);
     }
 }
 
@@ -159,6 +178,7 @@ __global__ void __launch_bounds__(32) k_xfer_bulk(const XferDesc *__restrict__ d
     }
     __syncwarp();
     if (threadIdx.x != 0) return;
+    ts_begin(g);
     const int32_t ppc = (int32_t)((g.chunk + piece - 1) / piece);   // pieces per chunk
     const int64_t K = (j1 - j0) * ppc;
     auto locate = [&](int64_t k, char *&src, char *&dst, uint32_t &bytes) {
@@ -204,6 +224,7 @@ __global__ void __launch_bounds__(32) k_xfer_bulk(const XferDesc *__restrict__ d
         }
     }
     bulk_wait_all();
+    ts_end(g);
 }
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {

@@ -26,6 +26,7 @@ struct XferGeom {
     int64_t n_pool;      // N
     int64_t chunk;       // C bytes (multiple of 16)
     int32_t two_l;       // 2L chunks per block
+    unsigned long long *ts = nullptr;   // optional {first CTA start, last CTA end} in %globaltimer ns (tc_timing)
 };
 
 // gather: ext[i] + lk*C  <-  kv + (lk*N + blk_i)*C      (a3: offload; epilogue table[tab_i] = -1)

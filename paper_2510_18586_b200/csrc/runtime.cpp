@@ -108,6 +108,7 @@ Pool::~Pool() {
     for (auto &kv_ : extra)
         if (kv_.second.host) cudaFreeHost(kv_.second.host);
     if (ring_host) cudaFreeHost(ring_host);
+    if (kts_dev) cudaFree(kts_dev);
 }
 
 tc_status Pool::create(const tc_pool_desc &d) {
@@ -275,6 +276,42 @@ void Pool::spans_collect() {
         tev_free.push_back(sp.b);
     }
     spans.clear();
+    if (!kts_meta.empty()) {                        // device-side kernel durations (%globaltimer)
+        const size_t used = kts_meta.size();
+        std::vector<unsigned long long> buf(2 * used);
+        if (cudaMemcpy(buf.data(), kts_dev, used * 16, cudaMemcpyDeviceToHost) == cudaSuccess) {
+            for (size_t i = 0; i < used; ++i) {
+                if (buf[2 * i + 1] < buf[2 * i]) continue;          // launch had no CTA with work
+                const int k = kts_meta[i].first;
+                tacc.kernel_ms[k] += (double)(buf[2 * i + 1] - buf[2 * i]) * 1e-6;
+                tacc.kernel_count[k] += 1;
+                tacc.kernel_bytes[k] += kts_meta[i].second;
+            }
+            cudaMemcpy(kts_dev, kts_init.data(), used * 16, cudaMemcpyHostToDevice);
+        } else {
+            cudaGetLastError();
+        }
+        kts_meta.clear();
+    }
+}
+
+// Kernel geometry for one launch; with tc_timing on, also a {start, end} %globaltimer slot for that launch.
+XferGeom Pool::geom(int32_t kind, int64_t bytes) {
+    XferGeom g{N, C, 2 * L, nullptr};
+    if (!timing || meta_only) return g;
+    if (!kts_dev) {
+        if (cudaMalloc(&kts_dev, (size_t)kKts * 16) != cudaSuccess) { cudaGetLastError(); kts_dev = nullptr; return g; }
+        kts_init.assign(2 * kKts, 0);
+        for (int64_t i = 0; i < kKts; ++i) kts_init[2 * i] = ~0ull;
+        if (cudaMemcpy(kts_dev, kts_init.data(), (size_t)kKts * 16, cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaGetLastError();
+            return g;
+        }
+    }
+    if ((int64_t)kts_meta.size() >= kKts) return g;      // more launches than slots before a sync: untimed
+    g.ts = kts_dev + 2 * kts_meta.size();
+    kts_meta.emplace_back(kind, bytes);
+    return g;
 }
 
 char *Pool::host_ptr(int64_t slot) const {
@@ -423,7 +460,7 @@ tc_status Pool::xfer_copy(XferJob &j, int64_t a, int64_t b, char *base) {
 // Device-side gather/scatter of pieces [a, b) against the staging slot `base`: descriptors by value in the kernel
 // parameters when they fit, else in the pinned descriptor ring.
 tc_status Pool::xfer_kernel(XferJob &j, int64_t a, int64_t b, char *base) {
-    const XferGeom g{N, C, 2 * L};
+    const XferGeom g = geom(j.gather ? 0 : 1, (b - a) * B);
     cudaEvent_t t0;
     tc_status s0;
     if (b - a <= kMaxInlineDesc) {
@@ -455,11 +492,11 @@ tc_status Pool::xfer_kernel(XferJob &j, int64_t a, int64_t b, char *base) {
 
 tc_status Pool::xfer_phase_a(XferJob &j) {
     if (j.n == 0) return TC_OK;
-    const XferGeom g{N, C, 2 * L};
     tc_status st;
     if (j.mode == TC_XFER_DIRECT) {
         const bool dev_tier = j.slot_of == nullptr || j.slot_of->empty();
         const int path = dev_tier ? 2 : (j.gather ? 0 : 1);
+        const XferGeom g = geom(dev_tier ? 2 : (j.gather ? 0 : 1), j.n * B);
         char *dptr = nullptr;
         char *h = ring_alloc(j.n * (int64_t)sizeof(XferDesc), &dptr);
         if (!h) return cuda_fail(cudaErrorMemoryAllocation, "descriptor ring");

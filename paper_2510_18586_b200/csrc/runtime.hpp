@@ -134,6 +134,11 @@ struct Pool {
     std::vector<tc_span_t> timeline;         // per-span records (tc_timeline), capped
     int64_t timeline_cap = 0;
     int64_t sync_count = 0;
+    static constexpr int64_t kKts = 4096;    // timed launches per sync interval
+    unsigned long long *kts_dev = nullptr;   // device {start, end} %globaltimer pairs, one per timed launch
+    std::vector<unsigned long long> kts_init;
+    std::vector<std::pair<int32_t, int64_t>> kts_meta;   // (kind, bytes) per used pair
+    XferGeom geom(int32_t kind, int64_t bytes);
     double cal_ms[2] = {0, 0};               // link-side transfer time per direction (tc_xfer_model_measure)
     int64_t cal_blocks[2] = {0, 0};
 
