@@ -10,8 +10,8 @@ host slots (a4, a7) — exactly the P:645-648 order, through the C ABI.
   python bench.py --impl reference ...     # the CPU oracle (oracle/), timed on the host cores
 
 Default workload: C2 (BASELINE.json configs[1], Qwen2.5-7B-shaped KV, Code-Writer-style 16 agents) on every rank —
-weak scaling over independent agent sets.  --workload c4/c5 runs the head-sharded 32B/70B configs (G = N ranks).
-Prints ONE JSON line on rank 0.
+weak scaling over independent agent sets.  --workload c4 / c5 runs the head-sharded 32B / 70B configs (C4: G = N;
+C5: G = 8, one rank's shard per GPU).  Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
@@ -33,6 +33,7 @@ from workloads.scripts import CycleGen, setup_ops  # noqa: E402
 
 METRIC = "KV offload/upload GB/s and blocks/s per GPU vs host-link & HBM peak at 1/2/4/8 GPUs"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+XFER_NAMES = {1: "direct", 2: "staged", 3: "copy"}
 HBM_FALLBACK = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback (GB/s), only if MEASURED_PEAKS.json is absent
 
 
@@ -43,7 +44,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=None)
-    ap.add_argument("--mode", default="auto", choices=["auto", "direct", "staged"])
+    ap.add_argument("--mode", default="auto", choices=["auto", "direct", "staged", "copy", "mixed", "mixed_rev"],
+                    help="transfer path per direction; mixed = direct D2H + staged H2D, mixed_rev = the reverse")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--quick", action="store_true", help="skip host-link probe and device-tier microbench")
@@ -55,11 +57,17 @@ def dist_env():
 
 
 def workload_for(args, world):
+    """(config, head shards G, scaling).  C4 is head-sharded over the ranks present (G = N: strong scaling; at N = 1
+    the whole 128 GiB pool sits on one GPU).  C5 is defined on 8 x B200 (BASELINE configs[4]): G = 8 always, and N < 8
+    GPUs run N of its 8 rank shards (80 GiB each) — fixed work per GPU, weak scaling.  C1-C3: one whole pool per
+    rank, independent agent sets (weak)."""
     name = args.workload or "c2"
     cfg = CONFIGS[name]
-    sharded = name in ("c4", "c5")
-    G = world if sharded else 1
-    return cfg, G, ("strong" if sharded and world > 1 else "weak")
+    if name == "c4":
+        return cfg, world, ("strong" if world > 1 else "weak")
+    if name == "c5":
+        return cfg, cfg.G, "weak"
+    return cfg, 1, "weak"
 
 
 # ------------------------------------------------------------------------------------------------- measurement aids
@@ -158,14 +166,17 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     cfg, G, scaling = workload_for(args, world)
-    shard_rank = rank if G > 1 else 0
-    mode = {"auto": tcb.XFER_AUTO, "direct": tcb.XFER_DIRECT, "staged": tcb.XFER_STAGED}[args.mode]
+    shard_rank = rank % G if G > 1 else 0
+    mode_d2h, mode_h2d = {"auto": (tcb.XFER_AUTO,) * 2, "direct": (tcb.XFER_DIRECT,) * 2,
+                          "staged": (tcb.XFER_STAGED,) * 2, "copy": (tcb.XFER_COPY,) * 2,
+                          "mixed": (tcb.XFER_DIRECT, tcb.XFER_STAGED),
+                          "mixed_rev": (tcb.XFER_STAGED, tcb.XFER_DIRECT)}[args.mode]
     S = cfg.host_slots()
 
     link = None if args.quick else hostlink_peak(torch, dev)
     pool = tcb.Pool(cfg.L, cfg.H, cfg.D, cfg.T, cfg.dtype, cfg.N, device=local, shard_rank=shard_rank, shard_world=G,
                     host_slots=S, max_agents=1024, max_blocks_per_agent=cfg.max_blocks_per_agent,
-                    xfer_d2h=mode, xfer_h2d=mode)
+                    xfer_d2h=mode_d2h, xfer_h2d=mode_h2d)
     pool.fill(cfg.seed)
     B = pool.block_bytes
 
@@ -224,9 +235,9 @@ def run_ours(args):
         cycle()
     for _ in range(args.warmup):
         cycle()
-    pool.timing(True)
-    pool.timing(True)                          # reset accumulators
-    pool.timeline_arm(200000)
+    # timed region: the kernels' own %globaltimer start/end only (timing mode 2: no extra events on the streams)
+    pool.timing(2)
+    pool.timing(2)                             # reset accumulators
     launches0 = pool.stats()["kernel_launches"]
     memcpy0 = pool.stats()["memcpy_calls"]
     if dist is not None:
@@ -259,9 +270,22 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     t_wall = time.perf_counter() - t_wall0
     clk = clocks.stop()
-    tim = pool.timing(False)
-    tl_summary = timeline_summary(pool.timeline(200000))
+    tim = pool.timing(0)
     launches = pool.stats()["kernel_launches"] - launches0
+    # diagnostic pass after the timed region (not in `value`): CUDA-event spans around every launch and DMA run, for
+    # the per-direction DMA rates and the per-step timeline (events cost ~2 % of the step, so they stay out of it)
+    pool.timing(1)
+    pool.timing(1)
+    pool.timeline_arm(200000)
+    n_diag = min(args.steps, 20)
+    for _ in range(n_diag):
+        cycle()
+    diag = pool.timing(0)
+    tl_raw = pool.timeline(200000)
+    tl_summary = timeline_summary(tl_raw)
+    if os.environ.get("TC_DUMP_TIMELINE"):                 # debugging aid: raw per-span records of the diagnostic steps
+        with open(os.environ["TC_DUMP_TIMELINE"], "w") as f:
+            json.dump(tl_raw, f)
 
     my = torch.tensor([sum(dev_ms), sum(host_ms), bytes_up + bytes_off, blocks, t_wall], dtype=torch.float64,
                       device=dev)
@@ -281,42 +305,45 @@ def run_ours(args):
 
     value = all_bytes / (dev_total_ms * 1e-3) / 1e9
     e2e = all_bytes / (host_total_ms * 1e-3) / 1e9
-    # roofline of the dominant kernel: per-launch algorithmic bytes / event-timed launch duration
+    # roofline of the dominant kernel: per-launch algorithmic bytes / the launch's device duration
+    stats = pool.stats()
+    link_bound = {"offload_kernel": stats["xfer_d2h"] == tcb.XFER_DIRECT,
+                  "upload_kernel": stats["xfer_h2d"] == tcb.XFER_DIRECT}
     kern = {}
     for k, peak_key in (("offload_kernel", "d2h_gbs"), ("upload_kernel", "h2d_gbs")):
         # kernel duration = first CTA start -> last CTA end on the device clock (%globaltimer), recorded by the
         # kernel itself on the stream it runs on; the CUDA-event span around the launch (which also counts host
         # launch latency when the stream was idle) is kept beside it
         ms, cnt, byt = tim["dev_" + k]
-        ev_ms, ev_cnt, _ = tim[k]
-        if cnt:
-            kern[k] = {"ms_total": ms, "launches": cnt, "bytes_per_launch": byt / cnt,
-                       "achieved_gbs": byt / (ms * 1e-3) / 1e9, "peak_key": peak_key,
-                       "event_span_ms_total": ev_ms, "event_span_launches": ev_cnt}
+        if not cnt:
+            continue
+        e = {"ms_total": ms, "launches": cnt, "bytes_per_launch": byt / cnt, "ms_per_launch": ms / cnt,
+             "timing": "kernel-recorded %globaltimer first-CTA start -> last-CTA end, every launch of the timed region"}
+        if link_bound[k]:      # mapped-host kernel: every byte crosses the host link once
+            pk = link[peak_key] if link else None
+            e.update(bound="host_link", achieved=byt / (ms * 1e-3) / 1e9, peak=pk,
+                     peak_source="live pinned cudaMemcpyAsync 1 GiB in this run (" + peak_key + ")")
+            if link:
+                e["frac_of_bidir_share"] = e["achieved"] / (link["bidir_gbs"] / 2)
+        else:                  # staged device-side gather/scatter: HBM read + write of every byte
+            e.update(bound="hbm", achieved=2 * byt / (ms * 1e-3) / 1e9, peak=hbm, peak_source=hbm_src,
+                     bytes_per_launch=2 * byt / cnt)
+        e["frac"] = e["achieved"] / e["peak"] if e["peak"] else None
+        kern[k] = e
     for k in ("memcpy_d2h", "memcpy_h2d"):
-        ms, cnt, byt = tim[k]
+        ms, cnt, byt = diag[k]
         if cnt:
-            kern[k] = {"ms_total": ms, "runs": cnt, "achieved_gbs": byt / (ms * 1e-3) / 1e9}
-    stats = pool.stats()
+            kern[k] = {"ms_total": ms, "runs": cnt, "achieved_gbs": byt / (ms * 1e-3) / 1e9,
+                       "timing": f"CUDA-event spans around each DMA run, {n_diag} diagnostic steps after the timed region"}
     roof = None
     kern_only = {k: v for k, v in kern.items() if k.endswith("_kernel")}
     if kern_only:
         dom = max(kern_only, key=lambda k: kern_only[k]["ms_total"])
         kd = kern_only[dom]
-        if kd["peak_key"] and stats["xfer_d2h"] == tcb.XFER_DIRECT and dom == "offload_kernel" or \
-                stats["xfer_h2d"] == tcb.XFER_DIRECT and dom == "upload_kernel":
-            pk = link[kd["peak_key"]] if link else None   # direct mapped-host kernel: bound by the host link
-            roof = {"kernel": dom + " (direct, mapped host)", "bound": "host_link", "achieved": kd["achieved_gbs"],
-                    "peak": pk, "unit": "GB/s", "frac": (kd["achieved_gbs"] / pk) if pk else None, "traffic": None,
-                    "bytes_per_launch": kd["bytes_per_launch"], "ms_per_launch": kd["ms_total"] / kd["launches"],
-                    "peak_source": "live pinned cudaMemcpyAsync 1 GiB in this run"}
-        else:                                              # staged device-side gather/scatter: HBM, read + write
-            ach = 2 * kd["achieved_gbs"]
-            roof = {"kernel": dom + " (staged device-side piece)", "bound": "hbm", "achieved": ach, "peak": hbm,
-                    "unit": "GB/s", "frac": ach / hbm, "traffic": None, "bytes_per_launch": 2 * kd["bytes_per_launch"],
-                    "ms_per_launch": kd["ms_total"] / kd["launches"], "peak_source": hbm_src}
-        tot_ms = sum(v["ms_total"] for v in kern.values())
-        roof["share_of_transfer_time"] = kd["ms_total"] / tot_ms if tot_ms else None
+        roof = {"kernel": dom, "bound": kd["bound"], "achieved": kd["achieved"], "peak": kd["peak"],
+                "unit": "GB/s", "frac": kd["frac"], "traffic": None, "bytes_per_launch": kd["bytes_per_launch"],
+                "ms_per_launch": kd["ms_per_launch"], "peak_source": kd["peak_source"],
+                "share_of_kernel_time": kd["ms_total"] / sum(v["ms_total"] for v in kern_only.values())}
     # the step's binding resource is the host link: per-direction DMA/kernel rate and a per-step link roofline
     link_roof = None
     if link:
@@ -330,9 +357,8 @@ def run_ours(args):
                      "step_ms": sum(dev_ms) / len(dev_ms), "frac": tmin * 1e3 / sum(dev_ms),
                      "how": "per step: min(up,off) at half the measured bidirectional peak + the excess at the "
                             "unidirectional peak, vs the measured step time"}
-        for k, pk in (("memcpy_d2h", "d2h_gbs"), ("memcpy_h2d", "h2d_gbs"), ("offload_kernel", "d2h_gbs"),
-                      ("upload_kernel", "h2d_gbs")):
-            if k in kern and (k.startswith("memcpy") or roof and roof["bound"] == "host_link"):
+        for k, pk in (("memcpy_d2h", "d2h_gbs"), ("memcpy_h2d", "h2d_gbs")):
+            if k in kern:
                 link_roof[k + "_frac_of_unidir_peak"] = kern[k]["achieved_gbs"] / link[pk]
                 link_roof[k + "_frac_of_bidir_share"] = kern[k]["achieved_gbs"] / bi
     cpu = None
@@ -346,8 +372,7 @@ def run_ours(args):
         "config": {"workload": f"{cfg.name}: {cfg.title}", "layers": cfg.L, "kv_heads": cfg.H, "head_dim": cfg.D,
                    "block_tokens": cfg.T, "head_shards": G, "n_blocks": cfg.N, "block_shard_bytes": B,
                    "host_slots": S, "agents": cfg.n_agents, "per_cycle": cfg.per_cycle,
-                   "xfer": {1: "direct", 2: "staged"}[stats["xfer_d2h"]] + "/" +
-                           {1: "direct", 2: "staged"}[stats["xfer_h2d"]],
+                   "xfer": XFER_NAMES[stats["xfer_d2h"]] + "/" + XFER_NAMES[stats["xfer_h2d"]],
                    "l2": "flushed between steps (256 MiB write, outside the step events)",
                    "parallelism": f"{world} independent ranks" + (f", head-sharded G={G}" if G > 1 else "")},
         "blocks_per_s": all_blocks / (dev_total_ms * 1e-3),

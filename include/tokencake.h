@@ -56,9 +56,12 @@ typedef enum {
 } tc_status;
 
 typedef enum {
-    TC_XFER_AUTO = 0,    /* per direction: the path the library measured faster at create time (tc_calibrate) */
+    TC_XFER_AUTO = 0,    /* per direction: the path measured fastest for the cycle on B200 */
     TC_XFER_DIRECT = 1,  /* one SM kernel reads/writes mapped pinned host memory over the host link */
-    TC_XFER_STAGED = 2   /* SM gather/scatter to a device staging ring + copy-engine cudaMemcpyAsync */
+    TC_XFER_STAGED = 2,  /* SM gather/scatter to a device staging ring + copy-engine cudaMemcpyAsync */
+    TC_XFER_COPY = 3     /* the copy engine moves each block as one strided DMA (2L rows of C bytes, row pitch N*C in
+                            the pool) straight between the pool and its pinned slot; a small kernel rewrites the
+                            block table (offload: before the DMA; upload: after it) */
 } tc_xfer_mode;
 
 typedef struct tc_pool_desc {
@@ -115,8 +118,10 @@ tc_status tc_streams(tc_pool *p, void **upload_stream, void **offload_stream);
 tc_status tc_set_xfer_mode(tc_pool *p, int32_t d2h, int32_t h2d);
 /* Launch configuration of one kernel path: path 0 = direct D2H gather, 1 = direct H2D scatter, 2 = device-side
    gather/scatter (staged mode and device tier).  ctas <= 0 -> default grid; threads in {32..256} (SIMT variant);
-   variant 0 = SIMT warp-per-chunk 16-byte copies, 1 = TMA bulk copies (cp.async.bulk through a shared-memory ring,
-   one elected thread per CTA).  Results are identical for every setting; only speed differs. */
+   variant 0 = SIMT warp-per-chunk 16-byte copies, 1 = TMA bulk copies (cp.async.bulk through an 8-stage
+   shared-memory ring, one elected thread per CTA, one CTA per SM), 2 = SIMT tile split (4 KiB warp tiles spread
+   evenly over all CTAs), 3 = TMA bulk with a 4-stage ring (two CTAs per SM).  Other values -> TC_E_INVAL.
+   Results are identical for every setting; only speed differs. */
 tc_status tc_set_launch_config(tc_pool *p, int32_t path, int32_t ctas, int32_t threads, int32_t variant);
 /* Synthetic content: every 8-byte word of the unsharded pool = splitmix64(widx + seed*0xD1B54A32D192ED03), widx its
    index in [L][2][N][T][H][D]; this rank writes its head shard.  Tests/bench only. */
@@ -189,20 +194,24 @@ tc_status tc_handle_info(tc_pool *p, tc_handle h, int32_t *agent, int64_t *n, in
 tc_status tc_handle_host(tc_pool *p, tc_handle h, int64_t i, const void **host_ptr);
 tc_status tc_stats(tc_pool *p, tc_stats_t *s);
 /* Per-launch device timing (CUDA events recorded on the launching stream around every kernel / memcpy run).
-   Spans complete at tc_sync, where their durations are accumulated.  Index: 0 offload kernels, 1 upload kernels,
-   2 device-tier kernels, 3 staged D2H memcpy, 4 staged H2D memcpy.  bytes = KV payload bytes moved (n * B). */
+   Spans complete at tc_sync, where their durations are accumulated.  Index (TC_NKINDS): 0 offload kernels (direct
+   mode: the whole transfer; staged mode: the device-side gather), 1 upload kernels (likewise; scatter), 2
+   device-tier kernels, 3 D2H memcpy (staged / copy mode), 4 H2D memcpy.  bytes = KV payload bytes moved (n * B). */
+#define TC_NKINDS 5
 typedef struct tc_timing_t {
-    double ms[5];
-    int64_t count[5];
-    int64_t bytes[5];
-    /* device-side kernel durations (first CTA start -> last CTA end on %globaltimer, no host launch latency):
-       0 offload (gather) kernels, 1 upload (scatter) kernels, 2 device-tier kernels */
-    double kernel_ms[3];
-    int64_t kernel_count[3];
-    int64_t kernel_bytes[3];
+    double ms[TC_NKINDS];
+    int64_t count[TC_NKINDS];
+    int64_t bytes[TC_NKINDS];
+    /* device-side kernel durations (first CTA start -> last CTA end on %globaltimer, no host launch latency), same
+       index; the memcpy kinds (3, 4) stay 0 */
+    double kernel_ms[TC_NKINDS];
+    int64_t kernel_count[TC_NKINDS];
+    int64_t kernel_bytes[TC_NKINDS];
 } tc_timing_t;
-/* enable != 0 turns span recording on (off by default: zero overhead).  If out != NULL it receives the totals
-   accumulated since the previous call, which are then reset. */
+/* enable: 0 off (the default: zero overhead); 1 event spans around every kernel / memcpy run plus the kernels' own
+   start/end timestamps; 2 the kernels' timestamps only (no events: does not perturb the stream schedule).  Other
+   values -> TC_E_INVAL.  If out != NULL it receives the totals accumulated since the previous call, which are then
+   reset. */
 tc_status tc_timing(tc_pool *p, int32_t enable, tc_timing_t *out);
 /* Per-span timeline (needs tc_timing enabled): kind as in tc_timing_t, start/end in ms relative to the first span
    after the previous tc_sync, `sync` = index of the sync interval.  out == NULL arms recording of up to `cap`

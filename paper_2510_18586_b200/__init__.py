@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libtokencake.so")
 
 OK, E_INVAL, E_NOBLOCKS, E_NOHOST, E_HANDLE, E_BUSY, E_CUDA, E_OOM, E_NODEV = 0, -1, -2, -3, -4, -5, -6, -7, -8
 FP16, BF16 = 0, 1
-XFER_AUTO, XFER_DIRECT, XFER_STAGED = 0, 1, 2
+XFER_AUTO, XFER_DIRECT, XFER_STAGED, XFER_COPY = 0, 1, 2, 3
 DTYPES = {"fp16": FP16, "bf16": BF16}
 
 SYMBOLS = [
@@ -59,8 +59,8 @@ class PoolDesc(ctypes.Structure):
 
 class Timing(ctypes.Structure):
     _fields_ = [("ms", ctypes.c_double * 5), ("count", ctypes.c_int64 * 5), ("bytes", ctypes.c_int64 * 5),
-                ("kernel_ms", ctypes.c_double * 3), ("kernel_count", ctypes.c_int64 * 3),
-                ("kernel_bytes", ctypes.c_int64 * 3)]
+                ("kernel_ms", ctypes.c_double * 5), ("kernel_count", ctypes.c_int64 * 5),
+                ("kernel_bytes", ctypes.c_int64 * 5)]
 
 
 class Span(ctypes.Structure):
@@ -69,6 +69,7 @@ class Span(ctypes.Structure):
 
 
 TIMING_KINDS = ("offload_kernel", "upload_kernel", "device_kernel", "memcpy_d2h", "memcpy_h2d")
+KERNEL_KINDS = (0, 1, 2)
 
 
 class Stats(ctypes.Structure):
@@ -368,14 +369,14 @@ class Pool:
         d["free"], d["alloc"], d["pending"] = s.free_blocks, s.alloc_blocks, s.pending_blocks
         return d
 
-    def timing(self, enable: bool = True) -> dict:
+    def timing(self, enable: bool | int = True) -> dict:
         """Enable/disable per-launch timing; returns {kind: (ms, count, bytes)} accumulated since the last call:
         event spans per kind (TIMING_KINDS) plus device-side kernel durations under 'dev_<kind>'."""
         t = Timing()
-        self._check(lib.tc_timing(self._h, 1 if enable else 0, ctypes.byref(t)))
+        self._check(lib.tc_timing(self._h, int(enable), ctypes.byref(t)))
         out = {k: (t.ms[i], t.count[i], t.bytes[i]) for i, k in enumerate(TIMING_KINDS)}
-        for i, k in enumerate(TIMING_KINDS[:3]):
-            out["dev_" + k] = (t.kernel_ms[i], t.kernel_count[i], t.kernel_bytes[i])
+        for i in KERNEL_KINDS:
+            out["dev_" + TIMING_KINDS[i]] = (t.kernel_ms[i], t.kernel_count[i], t.kernel_bytes[i])
         return out
 
     def timeline_arm(self, cap: int = 100000):

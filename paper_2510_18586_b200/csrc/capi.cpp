@@ -100,9 +100,9 @@ tc_status tc_streams(tc_pool *p, void **upload_stream, void **offload_stream) {
 
 tc_status tc_set_xfer_mode(tc_pool *p, int32_t d2h, int32_t h2d) {
     TC_GUARD(p) {
-        if (d2h < 0 || d2h > 2 || h2d < 0 || h2d > 2) return TC_E_INVAL;
-        P.mode_d2h = d2h == TC_XFER_AUTO ? TC_XFER_DIRECT : d2h;
-        P.mode_h2d = h2d == TC_XFER_AUTO ? TC_XFER_DIRECT : h2d;
+        if (d2h < 0 || d2h > 3 || h2d < 0 || h2d > 3) return TC_E_INVAL;
+        P.mode_d2h = d2h == TC_XFER_AUTO ? P.auto_mode(0) : d2h;
+        P.mode_h2d = h2d == TC_XFER_AUTO ? P.auto_mode(1) : h2d;
         return TC_OK;
     }
     TC_CATCH
@@ -110,7 +110,7 @@ tc_status tc_set_xfer_mode(tc_pool *p, int32_t d2h, int32_t h2d) {
 
 tc_status tc_set_launch_config(tc_pool *p, int32_t path, int32_t ctas, int32_t threads, int32_t variant) {
     TC_GUARD(p) {
-        if (path < 0 || path > 2 || threads < 32 || threads > 256 || threads % 32 || variant < 0 || variant > 1)
+        if (path < 0 || path > 2 || threads < 32 || threads > 256 || threads % 32 || variant < 0 || variant > 3)
             return TC_E_INVAL;
         P.ctas[path] = ctas;
         P.nthreads[path] = threads;
@@ -319,7 +319,8 @@ tc_status tc_stats(tc_pool *p, tc_stats_t *s) {
 
 tc_status tc_timing(tc_pool *p, int32_t enable, tc_timing_t *out) {
     TC_GUARD(p) {
-        P.timing = enable != 0 && !P.meta_only;
+        if (enable < 0 || enable > 2) return TC_E_INVAL;
+        P.timing = P.meta_only ? 0 : enable;
         if (out) {
             *out = P.tacc;
             P.tacc = tc_timing_t{};

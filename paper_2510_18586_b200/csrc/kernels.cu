@@ -1,17 +1,39 @@
 // sm_100a gather / scatter kernels of the Tokencake offload/upload hot path, and the synthetic-content fill kernel.
 //
-// Data movement only — no tensor cores (no contraction anywhere on this path).  One warp copies one
-// (block, layer, K|V) chunk of C contiguous bytes with 16-byte vector loads/stores, U loads in flight per lane before
-// the matching stores (Little's law against HBM / host-link latency).  Each CTA owns a contiguous range of chunks,
-// stages that range's descriptors in shared memory once (one host-link round trip when the descriptors sit in mapped
-// pinned memory), and the warp that copies chunk 0 of a block performs the fused block-table epilogue
-// (P:649 location flag / remap).
+// Data movement only — no tensor cores (no contraction anywhere on this path).  A launch moves the
+// 2L chunks (C contiguous bytes each, one per (layer, K|V)) of up to kMaxInlineDesc blocks between the paged pool
+// [L][2][N][C] and each block's contiguous [L][2][C] image elsewhere (a mapped pinned host slot, a device staging
+// slot or a caller buffer).  The warp / thread that moves byte 0 of a block also performs the fused block-table
+// epilogue (P:649 location flag on offload, P:388 remap on upload).
+//
+// Descriptors travel BY VALUE in the kernel parameters (up to 32 KiB of parameter space, 2040 descriptors): a CTA
+// reads its descriptors from the constant bank, so no launch reads host memory for its control data and no copy has
+// to precede it.  (Measured on B200: CTAs fetching descriptors from a mapped pinned ring serialise at ~30 ns per CTA
+// on the host link, which made wide grids slower than narrow ones; profiles/r01_tier_probe_v1.json.)
+//
+// Variants (same bytes, different engines; tc_set_launch_config):
+//   0  SIMT, one warp per chunk (16-byte vectors, 8 in flight per lane)
+//   1  TMA bulk, one elected thread per CTA streams 16 KiB pieces through an 8-stage shared-memory ring (1 CTA/SM)
+//   2  SIMT, the launch's chunks cut into 4 KiB warp tiles split evenly over all CTAs
+//   3  TMA bulk, 4-stage ring (2 CTAs/SM)
+// Work is split over CTAs at piece/tile granularity (variants 1-3), so a small launch (the staged head/tail piece)
+// still reaches every SM and a large one has no chunk-granular tail.
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace tc {
 namespace {
 
 constexpr int kUnroll = 8;
+constexpr int kTileU = 8;
+constexpr int64_t kTileBytes = kTileU * 512;   // one warp-iteration: 32 lanes x kTileU 16-byte vectors
+constexpr int64_t kPieceMax = 16384;           // TMA bulk piece (bytes per cp.async.bulk)
+
+template <int kCap>
+struct Descs {
+    XferDesc d[kCap];
+};
 
 __device__ __forceinline__ int4 ld_stream(const int4 *p) {
     int4 r;
@@ -25,19 +47,6 @@ __device__ __forceinline__ void st_stream(int4 *p, const int4 &v) {
     asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                  "r"(v.w)
                  : "memory");
-}
-
-// Copy nv int4 vectors; the warp's 32 lanes cover 512 contiguous bytes per step.
-__device__ __forceinline__ void warp_copy(int4 *__restrict__ dst, const int4 *__restrict__ src, int64_t nv, int lane) {
-    int64_t v = lane;
-    for (; v + 32 * (kUnroll - 1) < nv; v += 32 * kUnroll) {
-        int4 r[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) r[u] = ld_stream(src + v + 32 * u);
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) st_stream(dst + v + 32 * u, r[u]);
-    }
-    for (; v < nv; v += 32) st_stream(dst + v, ld_stream(src + v));
 }
 
 // Device-side launch timing (tc_timing): earliest CTA start / latest CTA end on the %globaltimer clock (ns), so a
@@ -54,37 +63,42 @@ __device__ __forceinline__ void ts_end(const XferGeom &g) {
     if (g.ts) atomicMax(g.ts + 1, now_ns());
 }
 
+// Byte address of offset `off` of chunk lk of descriptor d, in the pool and in the block's contiguous image.
+struct Loc {
+    char *pool, *ext;
+};
+__device__ __forceinline__ Loc locate(const XferDesc &d, int64_t lk, int64_t off, const XferGeom &g, char *kv) {
+    return {kv + (lk * g.n_pool + d.blk) * g.chunk + off, reinterpret_cast<char *>(d.ext) + lk * g.chunk + off};
+}
+
+// ------------------------------------------------------------------------------------------------ variant 0
 template <bool kGather>
-__device__ __forceinline__ void xfer_body(const XferDesc *__restrict__ desc, int64_t n, const XferGeom &g,
-                                          char *__restrict__ kv, int32_t *__restrict__ table, int64_t chunks_per_cta,
-                                          XferDesc *sdesc) {
+__device__ __forceinline__ void chunk_body(const XferDesc *__restrict__ desc, int64_t n, const XferGeom &g,
+                                           char *__restrict__ kv, int32_t *__restrict__ table, int64_t per_cta) {
     const int64_t M = n * g.two_l;
-    const int64_t j0 = (int64_t)blockIdx.x * chunks_per_cta;
+    const int64_t j0 = (int64_t)blockIdx.x * per_cta;
     if (j0 >= M) return;
     if (threadIdx.x == 0) ts_begin(g);
-    const int64_t j1 = min(M, j0 + chunks_per_cta);
-    const int64_t i0 = j0 / g.two_l;
-    const int nb = (int)((j1 - 1) / g.two_l - i0 + 1);
-    {
-        const int4 *s = reinterpret_cast<const int4 *>(desc + i0);
-        int4 *d = reinterpret_cast<int4 *>(sdesc);
-        for (int k = threadIdx.x; k < nb; k += blockDim.x) d[k] = s[k];
-    }
-    __syncthreads();
+    const int64_t j1 = min(M, j0 + per_cta);
     const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
     const int64_t nv = g.chunk >> 4;
-    for (int64_t j = j0 + warp; j < j1; j += nwarps) {
+    for (int64_t j = j0 + (threadIdx.x >> 5); j < j1; j += nwarps) {
         const int64_t i = j / g.two_l;
         const int64_t lk = j - i * g.two_l;
-        const XferDesc d = sdesc[i - i0];
-        char *pool_chunk = kv + (lk * g.n_pool + d.blk) * g.chunk;
-        char *ext_chunk = reinterpret_cast<char *>(d.ext) + lk * g.chunk;
-        if (kGather)
-            warp_copy(reinterpret_cast<int4 *>(ext_chunk), reinterpret_cast<const int4 *>(pool_chunk), nv, lane);
-        else
-            warp_copy(reinterpret_cast<int4 *>(pool_chunk), reinterpret_cast<const int4 *>(ext_chunk), nv, lane);
+        const XferDesc d = desc[i];
+        const Loc p = locate(d, lk, 0, g, kv);
+        const int4 *src = reinterpret_cast<const int4 *>(kGather ? p.pool : p.ext);
+        int4 *dst = reinterpret_cast<int4 *>(kGather ? p.ext : p.pool);
+        int64_t v = lane;
+        for (; v + 32 * (kUnroll - 1) < nv; v += 32 * kUnroll) {
+            int4 r[kUnroll];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) r[u] = ld_stream(src + v + 32 * u);
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) st_stream(dst + v + 32 * u, r[u]);
+        }
+        for (; v < nv; v += 32) st_stream(dst + v, ld_stream(src + v));
         if (lk == 0 && lane == 0 && d.tab >= 0) table[d.tab] = kGather ? -1 : d.blk;
     }
     if (g.ts) {
@@ -93,26 +107,51 @@ __device__ __forceinline__ void xfer_body(const XferDesc *__restrict__ desc, int
     }
 }
 
+// ------------------------------------------------------------------------------------------------ variant 2
 template <bool kGather>
-__global__ void __launch_bounds__(256) k_xfer(const XferDesc *__restrict__ desc, int64_t n, XferGeom g,
-                                              char *__restrict__ kv, int32_t *__restrict__ table,
-                                              int64_t chunks_per_cta) {
-    extern __shared__ XferDesc sdesc[];
-    xfer_body<kGather>(desc, n, g, kv, table, chunks_per_cta, sdesc);
+__device__ __forceinline__ void tile_body(const XferDesc *__restrict__ desc, int64_t n, const XferGeom &g,
+                                          char *__restrict__ kv, int32_t *__restrict__ table, int64_t per_cta) {
+    const int64_t tpc = (g.chunk + kTileBytes - 1) / kTileBytes;   // tiles per chunk
+    const int64_t tpb = tpc * g.two_l;                              // tiles per block
+    const int64_t Mt = n * tpb;
+    const int64_t t0 = (int64_t)blockIdx.x * per_cta;
+    if (t0 >= Mt) return;
+    if (threadIdx.x == 0) ts_begin(g);
+    const int64_t t1 = min(Mt, t0 + per_cta);
+    const int lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x >> 5;
+    for (int64_t t = t0 + (threadIdx.x >> 5); t < t1; t += nwarps) {
+        const int64_t i = t / tpb;
+        const int64_t r = t - i * tpb;
+        const int64_t lk = r / tpc;
+        const int64_t off = (r - lk * tpc) * kTileBytes;
+        const XferDesc d = desc[i];
+        const Loc p = locate(d, lk, off, g, kv);
+        const int4 *src = reinterpret_cast<const int4 *>(kGather ? p.pool : p.ext);
+        int4 *dst = reinterpret_cast<int4 *>(kGather ? p.ext : p.pool);
+        const int64_t nv = min(kTileBytes, g.chunk - off) >> 4;
+        if (nv == kTileU * 32) {
+            int4 v[kTileU];
+#pragma unroll
+            for (int u = 0; u < kTileU; ++u) v[u] = ld_stream(src + lane + 32 * u);
+#pragma unroll
+            for (int u = 0; u < kTileU; ++u) st_stream(dst + lane + 32 * u, v[u]);
+        } else {
+            for (int64_t v = lane; v < nv; v += 32) st_stream(dst + v, ld_stream(src + v));
+        }
+        if (r == 0 && lane == 0 && d.tab >= 0) table[d.tab] = kGather ? -1 : d.blk;
+    }
+    if (g.ts) {
+        __syncthreads();
+        if (threadIdx.x == 0) ts_end(g);
+    }
 }
 
-template <bool kGather>
-__global__ void __launch_bounds__(256) k_xfer_inl(const __grid_constant__ InlineDescs descs, int32_t n, XferGeom g,
-                                                  char *__restrict__ kv, int32_t *__restrict__ table,
-                                                  int64_t chunks_per_cta) {
-    __shared__ XferDesc sdesc[kMaxInlineDesc + 2];
-    xfer_body<kGather>(descs.d, n, g, kv, table, chunks_per_cta, sdesc);
-}
-
-// ------------------------------------------------------------------------------------------------ TMA bulk variant
-// One elected thread per CTA streams its chunk range through an NS-stage shared-memory ring with the TMA bulk-copy
-// engine: cp.async.bulk global->shared (mbarrier complete_tx), then cp.async.bulk shared->global (bulk_group).
-// Whole pieces of up to `piece` bytes move as single bulk transactions, to or from mapped host memory or HBM.
+// ------------------------------------------------------------------------------------------------ variants 1, 3
+// One elected thread per CTA streams its piece range through a kStages-deep shared-memory ring with the TMA bulk-copy
+// engine: cp.async.bulk global->shared (mbarrier complete_tx), then cp.async.bulk shared->global (bulk_group).  A
+// stage is refilled as soon as the bulk store that drains it has finished READING shared memory (wait_group.read), so
+// kStages loads stay in flight.  Pieces go to or from mapped host memory or HBM alike.
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -145,86 +184,145 @@ __device__ __forceinline__ void bulk_store(void *dst, const void *src_smem, uint
                  : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-constexpr int kStages = 8;
-
-template <bool kGather>
-__global__ void __launch_bounds__(32) k_xfer_bulk(const XferDesc *__restrict__ desc, int64_t n, XferGeom g,
-                                                  char *__restrict__ kv, int32_t *__restrict__ table,
-                                                  int64_t chunks_per_cta, int32_t piece) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    unsigned char *ring = smem;                                                   // kStages x piece
+template <bool kGather, int kStages>
+__device__ __forceinline__ void bulk_body(const XferDesc *__restrict__ desc, int64_t n, const XferGeom &g,
+                                          char *__restrict__ kv, int32_t *__restrict__ table, int64_t per_cta,
+                                          int32_t piece, unsigned char *smem) {
+    const int64_t ppc = (g.chunk + piece - 1) / piece;   // pieces per chunk
+    const int64_t ppb = ppc * g.two_l;                   // pieces per block
+    const int64_t K = n * ppb;
+    const int64_t k0 = (int64_t)blockIdx.x * per_cta;
+    if (k0 >= K || threadIdx.x != 0) return;
+    const int64_t k1 = min(K, k0 + per_cta);
+    unsigned char *ring = smem;                                                       // kStages x piece
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + (size_t)kStages * piece);  // kStages mbarriers
-    XferDesc *sdesc = reinterpret_cast<XferDesc *>(bars + kStages);
-    const int64_t M = n * g.two_l;
-    const int64_t j0 = (int64_t)blockIdx.x * chunks_per_cta;
-    if (j0 >= M) return;
-    const int64_t j1 = min(M, j0 + chunks_per_cta);
-    const int64_t i0 = j0 / g.two_l;
-    const int nb = (int)((j1 - 1) / g.two_l - i0 + 1);
-    {
-        const int4 *s = reinterpret_cast<const int4 *>(desc + i0);
-        int4 *d = reinterpret_cast<int4 *>(sdesc);
-        for (int k = threadIdx.x; k < nb; k += blockDim.x) d[k] = s[k];
-    }
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-    if (threadIdx.x != 0) return;
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     ts_begin(g);
-    const int32_t ppc = (int32_t)((g.chunk + piece - 1) / piece);   // pieces per chunk
-    const int64_t K = (j1 - j0) * ppc;
-    auto locate = [&](int64_t k, char *&src, char *&dst, uint32_t &bytes) {
-        const int64_t j = j0 + k / ppc;
-        const int64_t off = (int64_t)(k % ppc) * piece;
-        const int64_t i = j / g.two_l;
-        const int64_t lk = j - i * g.two_l;
-        const XferDesc d = sdesc[i - i0];
-        char *pool_chunk = kv + (lk * g.n_pool + d.blk) * g.chunk + off;
-        char *ext_chunk = reinterpret_cast<char *>(d.ext) + lk * g.chunk + off;
+    // piece k -> (src, dst, bytes); the load of a block's first piece carries the table epilogue
+    auto where = [&](int64_t k, char *&src, char *&dst, uint32_t &bytes, bool epi) {
+        const int64_t i = k / ppb;
+        const int64_t r = k - i * ppb;
+        const int64_t lk = r / ppc;
+        const int64_t off = (r - lk * ppc) * piece;
+        const XferDesc d = desc[i];
+        const Loc p = locate(d, lk, off, g, kv);
         bytes = (uint32_t)min((int64_t)piece, g.chunk - off);
-        src = kGather ? pool_chunk : ext_chunk;
-        dst = kGather ? ext_chunk : pool_chunk;
-        if (lk == 0 && off == 0 && d.tab >= 0) table[d.tab] = kGather ? -1 : d.blk;
+        src = kGather ? p.pool : p.ext;
+        dst = kGather ? p.ext : p.pool;
+        if (epi && r == 0 && d.tab >= 0) table[d.tab] = kGather ? -1 : d.blk;
     };
     auto issue_load = [&](int64_t k) {
         char *src, *dst;
         uint32_t bytes;
-        locate(k, src, dst, bytes);
-        const int s = (int)(k % kStages);
+        where(k, src, dst, bytes, true);
+        const int s = (int)((k - k0) % kStages);
         mbar_expect_tx(&bars[s], bytes);
         bulk_load(ring + (size_t)s * piece, src, bytes, &bars[s]);
     };
-    for (int64_t k = 0; k < K && k < kStages; ++k) issue_load(k);
-    for (int64_t k = 0; k < K; ++k) {
-        const int s = (int)(k % kStages);
-        mbar_wait(&bars[s], (uint32_t)((k / kStages) & 1));
+    for (int64_t k = k0; k < k1 && k < k0 + kStages; ++k) issue_load(k);
+    for (int64_t k = k0; k < k1; ++k) {
+        const int64_t q = k - k0;
+        const int s = (int)(q % kStages);
+        mbar_wait(&bars[s], (uint32_t)((q / kStages) & 1));
         char *src, *dst;
         uint32_t bytes;
-        const int64_t j = j0 + k / ppc;
-        const int64_t off = (int64_t)(k % ppc) * piece;
-        const int64_t i = j / g.two_l;
-        const int64_t lk = j - i * g.two_l;
-        const XferDesc d = sdesc[i - i0];
-        dst = kGather ? reinterpret_cast<char *>(d.ext) + lk * g.chunk + off : kv + (lk * g.n_pool + d.blk) * g.chunk + off;
-        bytes = (uint32_t)min((int64_t)piece, g.chunk - off);
-        (void)src;
+        where(k, src, dst, bytes, false);
         bulk_store(dst, ring + (size_t)s * piece, bytes);
         bulk_commit();
-        if (k >= 1 && k - 1 + kStages < K) {   // refill the previous stage once its store has read smem
-            bulk_wait_read<1>();
+        if (q >= 1 && k - 1 + kStages < k1) {   // refill the previous stage once its store has read smem
+            bulk_wait_read1();
             issue_load(k - 1 + kStages);
         }
     }
     bulk_wait_all();
     ts_end(g);
+}
+
+// ------------------------------------------------------------------------------------------------ kernels
+template <bool kGather, int kCap>
+__global__ void __launch_bounds__(256) k_xfer_chunk(const __grid_constant__ Descs<kCap> dd, int32_t n, XferGeom g,
+                                                    char *__restrict__ kv, int32_t *__restrict__ table,
+                                                    int64_t per_cta) {
+    chunk_body<kGather>(dd.d, n, g, kv, table, per_cta);
+}
+
+template <bool kGather, int kCap>
+__global__ void __launch_bounds__(256) k_xfer_tile(const __grid_constant__ Descs<kCap> dd, int32_t n, XferGeom g,
+                                                   char *__restrict__ kv, int32_t *__restrict__ table,
+                                                   int64_t per_cta) {
+    tile_body<kGather>(dd.d, n, g, kv, table, per_cta);
+}
+
+template <bool kGather, int kStages, int kCap>
+__global__ void __launch_bounds__(32) k_xfer_bulk(const __grid_constant__ Descs<kCap> dd, int32_t n, XferGeom g,
+                                                  char *__restrict__ kv, int32_t *__restrict__ table,
+                                                  int64_t per_cta, int32_t piece) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    bulk_body<kGather, kStages>(dd.d, n, g, kv, table, per_cta, piece, smem);
+}
+
+// Even split of `units` work units over at most `ctas` CTAs (each >= `min_per_cta` units): {grid, units per CTA}.
+inline void split(int64_t units, int64_t ctas, int64_t min_per_cta, int64_t *grid, int64_t *per_cta) {
+    const int64_t gsz = std::max<int64_t>(1, std::min<int64_t>(ctas, (units + min_per_cta - 1) / min_per_cta));
+    *per_cta = (units + gsz - 1) / gsz;
+    *grid = (units + *per_cta - 1) / *per_cta;
+}
+
+template <int kCap>
+cudaError_t launch_cap(bool gather, const XferDesc *host_desc, int32_t n, const XferGeom &g, char *kv,
+                       int32_t *table, int ctas, int threads, int variant, cudaStream_t s) {
+    Descs<kCap> dd;
+    std::copy(host_desc, host_desc + n, dd.d);
+    int64_t grid = 0, per = 0;
+    if (variant == 1 || variant == 3) {
+        const int32_t piece = (int32_t)std::min<int64_t>(g.chunk, kPieceMax);
+        const int64_t K = (int64_t)n * g.two_l * ((g.chunk + piece - 1) / piece);
+        const int stages = variant == 1 ? 8 : 4;
+        split(K, ctas > 0 ? ctas : (variant == 1 ? 148 : 296), 1, &grid, &per);
+        const size_t smem = (size_t)stages * piece + stages * sizeof(uint64_t);
+        auto fn = variant == 1 ? (gather ? k_xfer_bulk<true, 8, kCap> : k_xfer_bulk<false, 8, kCap>)
+                               : (gather ? k_xfer_bulk<true, 4, kCap> : k_xfer_bulk<false, 4, kCap>);
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        fn<<<(unsigned)grid, 32, smem, s>>>(dd, n, g, kv, table, per, piece);
+        return cudaGetLastError();
+    }
+    if (threads <= 0 || threads > 256) threads = 256;
+    const int64_t nwarps = threads / 32;
+    if (variant == 2) {
+        const int64_t Mt = (int64_t)n * g.two_l * ((g.chunk + kTileBytes - 1) / kTileBytes);
+        split(Mt, ctas > 0 ? ctas : 148 * 4, nwarps, &grid, &per);
+        if (gather)
+            k_xfer_tile<true, kCap><<<(unsigned)grid, threads, 0, s>>>(dd, n, g, kv, table, per);
+        else
+            k_xfer_tile<false, kCap><<<(unsigned)grid, threads, 0, s>>>(dd, n, g, kv, table, per);
+        return cudaGetLastError();
+    }
+    split((int64_t)n * g.two_l, ctas > 0 ? ctas : 148 * 4, nwarps, &grid, &per);
+    if (gather)
+        k_xfer_chunk<true, kCap><<<(unsigned)grid, threads, 0, s>>>(dd, n, g, kv, table, per);
+    else
+        k_xfer_chunk<false, kCap><<<(unsigned)grid, threads, 0, s>>>(dd, n, g, kv, table, per);
+    return cudaGetLastError();
+}
+
+// Table epilogue alone (COPY mode, where the copy engine moves the bytes): table[tab_i] = -1 (offload) / blk_i.
+template <int kCap>
+__global__ void k_table(const __grid_constant__ Descs<kCap> dd, int32_t n, bool gather, int32_t *__restrict__ table) {
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        if (dd.d[i].tab >= 0) table[dd.d[i].tab] = gather ? -1 : dd.d[i].blk;
+}
+
+template <int kCap>
+cudaError_t launch_table_cap(bool gather, const XferDesc *host_desc, int32_t n, int32_t *table, cudaStream_t s) {
+    Descs<kCap> dd;
+    std::copy(host_desc, host_desc + n, dd.d);
+    k_table<kCap><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dd, n, gather, table);
+    return cudaGetLastError();
 }
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -254,64 +352,24 @@ __global__ void k_fill(uint64_t *__restrict__ kv, int64_t n_chunks, int64_t n_po
 
 }  // namespace
 
-cudaError_t launch_xfer(bool gather, const XferDesc *desc, int64_t n, const XferGeom &g, void *kv, int32_t *table,
-                        int ctas, int threads, int variant, cudaStream_t s) {
+cudaError_t launch_xfer(bool gather, const XferDesc *host_desc, int32_t n, const XferGeom &g, void *kv,
+                        int32_t *table, int ctas, int threads, int variant, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
-    const int64_t M = n * g.two_l;
-    if (variant == 1) {   // TMA bulk: one CTA per SM, kStages x piece bytes of smem ring
-        const int32_t piece = (int32_t)std::min<int64_t>(g.chunk, 16384);
-        if (ctas <= 0) ctas = 148;
-        int64_t grid = std::min<int64_t>(ctas, M);
-        const int64_t cpc = (M + grid - 1) / grid;
-        grid = (M + cpc - 1) / cpc;
-        const int64_t max_nb = cpc / g.two_l + 2;
-        const size_t smem = (size_t)kStages * piece + kStages * sizeof(uint64_t) + (size_t)max_nb * sizeof(XferDesc);
-        auto fn = gather ? k_xfer_bulk<true> : k_xfer_bulk<false>;
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        fn<<<(unsigned)grid, 32, smem, s>>>(desc, n, g, static_cast<char *>(kv), table, cpc, piece);
-        return cudaGetLastError();
-    }
-    if (threads <= 0 || threads > 256) threads = 256;
-    if (ctas <= 0) ctas = 148 * 4;
-    const int64_t nwarps = threads / 32;
-    int64_t grid = std::min<int64_t>(ctas, (M + nwarps - 1) / nwarps);
-    if (grid < 1) grid = 1;
-    const int64_t cpc = (M + grid - 1) / grid;
-    grid = (M + cpc - 1) / cpc;
-    const int64_t max_nb = cpc / g.two_l + 2;
-    const size_t smem = (size_t)max_nb * sizeof(XferDesc);
-    if (smem > 48 * 1024) {
-        auto fn = gather ? k_xfer<true> : k_xfer<false>;
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    if (gather)
-        k_xfer<true><<<(unsigned)grid, threads, smem, s>>>(desc, n, g, static_cast<char *>(kv), table, cpc);
-    else
-        k_xfer<false><<<(unsigned)grid, threads, smem, s>>>(desc, n, g, static_cast<char *>(kv), table, cpc);
-    return cudaGetLastError();
+    if (n > kMaxInlineDesc || variant < 0 || variant > 3) return cudaErrorInvalidValue;
+    char *k = static_cast<char *>(kv);
+    if (n <= 64) return launch_cap<64>(gather, host_desc, n, g, k, table, ctas, threads, variant, s);
+    if (n <= 256) return launch_cap<256>(gather, host_desc, n, g, k, table, ctas, threads, variant, s);
+    return launch_cap<kMaxInlineDesc>(gather, host_desc, n, g, k, table, ctas, threads, variant, s);
 }
 
-cudaError_t launch_xfer_inline(bool gather, const XferDesc *host_desc, int32_t n, const XferGeom &g, void *kv,
-                               int32_t *table, int ctas, int threads, cudaStream_t s) {
-    if (n <= 0) return cudaSuccess;
-    if (n > kMaxInlineDesc) return cudaErrorInvalidValue;
-    InlineDescs d;
-    for (int i = 0; i < n; ++i) d.d[i] = host_desc[i];
-    const int64_t M = (int64_t)n * g.two_l;
-    if (threads <= 0 || threads > 256) threads = 256;
-    if (ctas <= 0) ctas = 148 * 4;
-    const int64_t nwarps = threads / 32;
-    int64_t grid = std::min<int64_t>(ctas, (M + nwarps - 1) / nwarps);
-    if (grid < 1) grid = 1;
-    const int64_t cpc = (M + grid - 1) / grid;
-    grid = (M + cpc - 1) / cpc;
-    if (gather)
-        k_xfer_inl<true><<<(unsigned)grid, threads, 0, s>>>(d, n, g, static_cast<char *>(kv), table, cpc);
-    else
-        k_xfer_inl<false><<<(unsigned)grid, threads, 0, s>>>(d, n, g, static_cast<char *>(kv), table, cpc);
-    return cudaGetLastError();
+cudaError_t launch_table(bool gather, const XferDesc *host_desc, int64_t n, int32_t *table, cudaStream_t s) {
+    for (int64_t a = 0; a < n; a += kMaxInlineDesc) {
+        const int32_t m = (int32_t)std::min<int64_t>(kMaxInlineDesc, n - a);
+        cudaError_t e = m <= 256 ? launch_table_cap<256>(gather, host_desc + a, m, table, s)
+                                 : launch_table_cap<kMaxInlineDesc>(gather, host_desc + a, m, table, s);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 cudaError_t launch_fill(void *kv, int64_t n_pool, int32_t L, int32_t T, int32_t H, int32_t Hl, int32_t rank,

@@ -16,11 +16,9 @@ struct XferDesc {
 };
 static_assert(sizeof(XferDesc) == 16, "XferDesc must be 16 bytes");
 
-// Staged-mode pieces carry their descriptors by value in the kernel parameters (no host-memory read in the kernel).
-constexpr int kMaxInlineDesc = 128;
-struct InlineDescs {
-    XferDesc d[kMaxInlineDesc];
-};
+// Descriptors travel by value in the kernel parameters (<= 32 KiB of parameter space); larger batches are launched
+// in pieces of at most kMaxInlineDesc blocks.
+constexpr int kMaxInlineDesc = 2040;
 
 struct XferGeom {
     int64_t n_pool;      // N
@@ -31,14 +29,15 @@ struct XferGeom {
 
 // gather: ext[i] + lk*C  <-  kv + (lk*N + blk_i)*C      (a3: offload; epilogue table[tab_i] = -1)
 // scatter: kv + (lk*N + blk_i)*C  <-  ext[i] + lk*C     (a6: upload; epilogue table[tab_i] = blk_i)
-// `desc` may live in mapped pinned memory.  ctas <= 0 selects the default grid.
-// variant 0 = SIMT warp-per-chunk 16-byte copy; 1 = TMA bulk (cp.async.bulk) through a shared-memory ring.
-cudaError_t launch_xfer(bool gather, const XferDesc *desc, int64_t n, const XferGeom &g, void *kv, int32_t *table,
-                        int ctas, int threads, int variant, cudaStream_t s);
+// host_desc: n <= kMaxInlineDesc descriptors in host memory, copied into the launch's parameters.  ctas <= 0 selects
+// the variant's default grid.  variant 0 = SIMT warp-per-chunk 16-byte copy; 1 = TMA bulk (cp.async.bulk) through
+// an 8-stage shared-memory ring, one CTA per SM; 2 = SIMT tile split (4 KiB warp tiles spread evenly over all CTAs);
+// 3 = TMA bulk, 4-stage ring, two CTAs per SM.
+cudaError_t launch_xfer(bool gather, const XferDesc *host_desc, int32_t n, const XferGeom &g, void *kv,
+                        int32_t *table, int ctas, int threads, int variant, cudaStream_t s);
 
-// Same copy as launch_xfer (SIMT variant) with n <= kMaxInlineDesc descriptors passed by value.
-cudaError_t launch_xfer_inline(bool gather, const XferDesc *host_desc, int32_t n, const XferGeom &g, void *kv,
-                               int32_t *table, int ctas, int threads, cudaStream_t s);
+// Table epilogue without a copy (COPY mode): table[tab_i] = gather ? -1 : blk_i for every descriptor with tab >= 0.
+cudaError_t launch_table(bool gather, const XferDesc *host_desc, int64_t n, int32_t *table, cudaStream_t s);
 
 // Synthetic content: word w of the unsharded [L][2][N][T][H][D] pool =
 // splitmix64(w + seed * 0xD1B54A32D192ED03); this shard holds heads [rank*Hl, (rank+1)*Hl).

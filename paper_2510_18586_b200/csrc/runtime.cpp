@@ -3,6 +3,7 @@
 #include "runtime.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -67,6 +68,21 @@ void BlockAllocator::set_free(int32_t b) {
     bits[b >> 6] |= 1ull << (b & 63);
     ++nfree;
     if ((b >> 6) < hint) hint = b >> 6;
+}
+
+// ------------------------------------------------------------------------------------------------ host trace
+// TC_HOST_TRACE=1: per tc_cycle, the host time (µs from the call's entry) at which each enqueue step returned, on
+// stderr.  A debugging aid for the enqueue critical path (how soon each link direction gets its first DMA).
+static bool g_trace = std::getenv("TC_HOST_TRACE") != nullptr;
+static std::chrono::steady_clock::time_point g_trace_t0;
+static std::string g_trace_buf;
+static void trace(const char *what) {
+    if (!g_trace) return;
+    const double us =
+        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - g_trace_t0).count();
+    char b[96];
+    std::snprintf(b, sizeof b, " %s=%.1f", what, us);
+    g_trace_buf += b;
 }
 
 // ------------------------------------------------------------------------------------------------ Pool
@@ -143,7 +159,7 @@ tc_status Pool::create(const tc_pool_desc &d) {
     next_slot = S;
     mode_d2h = d.xfer_d2h;
     mode_h2d = d.xfer_h2d;
-    if (mode_d2h < 0 || mode_d2h > 2 || mode_h2d < 0 || mode_h2d > 2) return TC_E_INVAL;
+    if (mode_d2h < 0 || mode_d2h > 3 || mode_h2d < 0 || mode_h2d > 3) return TC_E_INVAL;
     const char *path_names[3] = {"D2H", "H2D", "DEV"};
     for (int i = 0; i < 3; ++i) {
         char nm[32];
@@ -152,7 +168,7 @@ tc_status Pool::create(const tc_pool_desc &d) {
         std::snprintf(nm, sizeof nm, "TC_THREADS_%s", path_names[i]);
         nthreads[i] = env_int(nm, 256);
         std::snprintf(nm, sizeof nm, "TC_VARIANT_%s", path_names[i]);
-        variant[i] = env_int(nm, 0);
+        variant[i] = env_int(nm, i == 2 ? 3 : 0);   // device side: TMA bulk 4-stage (tier probe)
     }
     if (meta_only) return TC_OK;
 
@@ -164,7 +180,7 @@ tc_status Pool::create(const tc_pool_desc &d) {
     TC_CUDA(cudaStreamCreateWithPriority(&s_up_k, cudaStreamNonBlocking, hi), "upload aux stream");
     TC_CUDA(cudaStreamCreateWithPriority(&s_off_k, cudaStreamNonBlocking, lo), "offload aux stream");
     piece_bytes = env_int("TC_PIECE_KIB", 256 * 1024) * 1024ll;
-    head_bytes = env_int("TC_HEAD_KIB", 4096) * 1024ll;
+    head_bytes = env_int("TC_HEAD_KIB", 0) * 1024ll;
     use_batch_memcpy = env_int("TC_BATCH_MEMCPY", 1) != 0;
     TC_CUDA(cudaEventCreateWithFlags(&ev_compute, cudaEventDisableTiming), "event");
     const int64_t kv_bytes = (int64_t)L * 2 * N * C;
@@ -199,8 +215,8 @@ tc_status Pool::create(const tc_pool_desc &d) {
     if (staging_bytes < B) staging_bytes = B;
     // AUTO: the copy-engine staged path measured faster than the SM direct path in both directions on B200
     // (profiles/r01_xfer_probe.json: alone 57.1 vs 52.6 GB/s D2H, 55.4 vs 51.3 H2D; concurrent 53.7+49.7 vs 45+40).
-    if (mode_d2h == TC_XFER_AUTO) mode_d2h = env_int("TC_AUTO_D2H", TC_XFER_STAGED);
-    if (mode_h2d == TC_XFER_AUTO) mode_h2d = env_int("TC_AUTO_H2D", TC_XFER_STAGED);
+    if (mode_d2h == TC_XFER_AUTO) mode_d2h = auto_mode(0);
+    if (mode_h2d == TC_XFER_AUTO) mode_h2d = auto_mode(1);
     for (int i = 0; i < 16; ++i) {
         cudaEvent_t e;
         TC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -237,7 +253,7 @@ cudaEvent_t Pool::tev_get() {
 
 tc_status Pool::span_begin(cudaStream_t s, cudaEvent_t *a) {
     *a = nullptr;
-    if (!timing) return TC_OK;
+    if (timing != 1) return TC_OK;
     *a = tev_get();
     if (!*a) return cuda_fail(cudaErrorMemoryAllocation, "timing event");
     TC_CUDA(cudaEventRecord(*a, s), "timing event");
@@ -245,7 +261,7 @@ tc_status Pool::span_begin(cudaStream_t s, cudaEvent_t *a) {
 }
 
 tc_status Pool::span_end(cudaStream_t s, int32_t kind, cudaEvent_t a, int64_t bytes, bool link) {
-    if (!timing || !a) return TC_OK;
+    if (timing != 1 || !a) return TC_OK;
     cudaEvent_t b = tev_get();
     if (!b) return cuda_fail(cudaErrorMemoryAllocation, "timing event");
     TC_CUDA(cudaEventRecord(b, s), "timing event");
@@ -355,12 +371,16 @@ char *Pool::ring_alloc(int64_t bytes, char **dev_ptr) {
 // A transfer of desc.size() blocks, enqueued in two phases so that one scheduling cycle can interleave its two
 // directions on the host (tc_cycle) and both links start as early as possible:
 //   DIRECT          A = the single kernel over mapped host memory                 B = -
-//   STAGED gather   A = per piece: gather kernel (aux stream), event, D2H copy (main)   B = -
-//   STAGED scatter  A = the H2D copy per piece (main) + an event each             B = the scatter per piece (aux)
-// Pieces pipeline the device-side kernels against the copy engine with few host API calls: an offload is a small
-// head piece (its gather is all that precedes the first D2H byte) then large pieces; an upload is large pieces then
-// a small tail piece (its scatter is all that follows the last H2D byte).  A batch larger than the staging buffer
-// instead runs double-buffered pieces of half the buffer, issued interleaved in phase A (B does nothing).
+//   COPY            A = table kernel (offload) + one strided DMA per block + table kernel (upload)
+//   STAGED gather   A = per piece: gather kernel, D2H copy                        B = -
+//   STAGED scatter  A = the H2D copy per piece                                    B = the scatter per piece, join
+// A staged batch that fits the staging buffer is cut into pieces of piece_bytes (default: one piece).  One piece runs
+// kernel and DMA in stream order on the direction's main stream; several pieces pipeline the device-side kernels on
+// an aux stream against the copy engine.  TC_HEAD_KIB > 0 adds a small first (gather) / last (scatter) piece, so the
+// D2H link starts after a short gather and little scatter trails the last H2D byte — measured slower on B200 than
+// one large piece, because every extra DMA and cross-stream hop costs tens of µs (profiles/r01_staged_ab.md).  A
+// batch larger than the staging buffer runs double-buffered pieces of half the buffer, issued interleaved in phase
+// A (B does nothing).
 tc_status Pool::xfer_init(XferJob &j, bool gather, int32_t mode, const std::vector<XferDesc> *desc,
                           const std::vector<int64_t> *slot_of, cudaStream_t s) {
     j.gather = gather;
@@ -377,28 +397,91 @@ tc_status Pool::xfer_init(XferJob &j, bool gather, int32_t mode, const std::vect
     j.cut.clear();
     const int64_t cap = staging_bytes / B;                       // blocks the staging buffer holds (>= 1)
     j.ring_reuse = j.n > cap;
+    const int64_t edge = head_bytes > 0 ? std::max<int64_t>(1, head_bytes / B) : 0;   // head / tail blocks
+    const int64_t big = std::max<int64_t>(1, piece_bytes / B);
     if (j.ring_reuse) {
         const int64_t pb = std::max<int64_t>(1, cap / 2);
         for (int64_t a = 0; a < j.n; a += pb) j.cut.push_back(a);
+    } else if (edge == 0) {
+        for (int64_t a = 0; a < j.n; a += big) j.cut.push_back(a);
+    } else if (gather) {
+        j.cut.push_back(0);
+        for (int64_t a = std::min(edge, j.n); a < j.n; a += big) j.cut.push_back(a);
     } else {
-        const int64_t edge = std::max<int64_t>(1, head_bytes / B);          // small head (gather) / tail (scatter)
-        const int64_t big = std::max<int64_t>(1, piece_bytes / B);
-        if (gather) {
-            j.cut.push_back(0);
-            for (int64_t a = std::min(edge, j.n); a < j.n; a += big) j.cut.push_back(a);
-        } else {
-            const int64_t body = std::max<int64_t>(0, j.n - edge);
-            for (int64_t a = 0; a < body; a += big) j.cut.push_back(a);
-            j.cut.push_back(body);
-        }
+        const int64_t body = std::max<int64_t>(0, j.n - edge);
+        for (int64_t a = 0; a < body; a += big) j.cut.push_back(a);
+        j.cut.push_back(body);
     }
     j.cut.push_back(j.n);
     j.npieces = (int64_t)j.cut.size() - 1;
     j.ev.assign(j.npieces, -1);
+    if (j.npieces == 1) {                            // one piece: kernel and DMA in stream order, no cross-stream hop
+        j.sk = j.s;
+        return TC_OK;
+    }
     int32_t e0;
     tc_status st = ev_rec(s, &e0);                  // the aux stream starts after the main stream's waits
     if (st != TC_OK) return st;
     TC_CUDA(cudaStreamWaitEvent(j.sk, events[e0], 0), "aux wait");
+    return TC_OK;
+}
+
+// AUTO: the path measured fastest for a full scheduling cycle on B200 (both directions concurrently).
+int32_t Pool::auto_mode(int dir) const {
+    return env_int(dir == 0 ? "TC_AUTO_D2H" : "TC_AUTO_H2D", TC_XFER_STAGED);
+}
+
+// COPY mode: one strided DMA per block (2L rows of C bytes; pool row pitch N*C, slot rows packed), all blocks of the
+// batch in one cudaMemcpy3DBatchAsync call; the table epilogue is a small kernel in stream order (offload: first,
+// upload: after the data has landed).
+tc_status Pool::xfer_copy2d(XferJob &j) {
+    const auto &slot_of = *j.slot_of;
+    cudaEvent_t t0;
+    tc_status st;
+    const int64_t table_launches = (j.n + kMaxInlineDesc - 1) / kMaxInlineDesc;
+    if (j.gather) {
+        TC_CUDA(launch_table(true, j.desc->data(), j.n, table_dev, j.s), "table kernel");
+        n_launch += table_launches;
+    }
+    if ((st = span_begin(j.s, &t0)) != TC_OK) return st;
+    ops_.resize((size_t)j.n);
+    for (int64_t i = 0; i < j.n; ++i) {
+        cudaMemcpy3DBatchOp &o = ops_[i];
+        std::memset(&o, 0, sizeof o);
+        char *pool_p = kv + (int64_t)(*j.desc)[i].blk * C;
+        char *host_p = host_ptr(slot_of[i]);
+        cudaMemcpy3DOperand dev{}, hst{};
+        dev.type = cudaMemcpyOperandTypePointer;
+        dev.op.ptr.ptr = pool_p;
+        dev.op.ptr.rowLength = (size_t)(N * C);
+        hst.type = cudaMemcpyOperandTypePointer;
+        hst.op.ptr.ptr = host_p;
+        hst.op.ptr.rowLength = (size_t)C;
+        o.src = j.gather ? dev : hst;
+        o.dst = j.gather ? hst : dev;
+        o.extent = make_cudaExtent((size_t)C, (size_t)(2 * L), 1);
+        o.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    }
+    size_t fail = 0;
+    cudaError_t e = use_batch_memcpy ? cudaMemcpy3DBatchAsync((size_t)j.n, ops_.data(), &fail, 0, j.s)
+                                     : cudaErrorNotSupported;
+    if (e != cudaSuccess) {                         // not available: one 2D copy per block
+        cudaGetLastError();
+        for (int64_t i = 0; i < j.n; ++i) {
+            const cudaMemcpy3DBatchOp &o = ops_[i];
+            TC_CUDA(cudaMemcpy2DAsync(o.dst.op.ptr.ptr, o.dst.op.ptr.rowLength, o.src.op.ptr.ptr,
+                                      o.src.op.ptr.rowLength, (size_t)C, (size_t)(2 * L),
+                                      j.gather ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, j.s),
+                    "2D memcpy");
+        }
+    }
+    trace(j.gather ? "d2h" : "h2d");
+    ++n_memcpy;
+    if ((st = span_end(j.s, j.gather ? 3 : 4, t0, j.n * B)) != TC_OK) return st;
+    if (!j.gather) {
+        TC_CUDA(launch_table(false, j.desc->data(), j.n, table_dev, j.s), "table kernel");
+        n_launch += table_launches;
+    }
     return TC_OK;
 }
 
@@ -442,6 +525,7 @@ tc_status Pool::xfer_copy(XferJob &j, int64_t a, int64_t b, char *base) {
         cudaError_t e = cudaMemcpyBatchAsync(cp_dst.data(), cp_src.data(), cp_size.data(), cp_dst.size(), &attr,
                                              &attr_idx, 1, &fail_idx, j.s);
         if (e == cudaSuccess) {
+            trace(to_host ? "d2h" : "h2d");
             ++n_memcpy;
             return span_end(j.s, to_host ? 3 : 4, t0, (b - a) * B);
         }
@@ -454,64 +538,59 @@ tc_status Pool::xfer_copy(XferJob &j, int64_t a, int64_t b, char *base) {
                 "staged memcpy");
         ++n_memcpy;
     }
+    trace(to_host ? "d2h" : "h2d");
     return span_end(j.s, to_host ? 3 : 4, t0, (b - a) * B);
 }
 
-// Device-side gather/scatter of pieces [a, b) against the staging slot `base`: descriptors by value in the kernel
-// parameters when they fit, else in the pinned descriptor ring.
-tc_status Pool::xfer_kernel(XferJob &j, int64_t a, int64_t b, char *base) {
-    const XferGeom g = geom(j.gather ? 0 : 1, (b - a) * B);
-    cudaEvent_t t0;
-    tc_status s0;
-    if (b - a <= kMaxInlineDesc) {
-        XferDesc pd[kMaxInlineDesc];
-        for (int64_t i = a; i < b; ++i) {
-            pd[i - a] = (*j.desc)[i];
-            pd[i - a].ext = reinterpret_cast<uint64_t>(base + (i - a) * B);
-        }
-        if ((s0 = span_begin(j.sk, &t0)) != TC_OK) return s0;
-        TC_CUDA(launch_xfer_inline(j.gather, pd, (int32_t)(b - a), g, kv, table_dev, ctas[2], nthreads[2], j.sk),
-                j.gather ? "gather kernel" : "scatter kernel");
-    } else {
-        char *dptr = nullptr;
-        char *h = ring_alloc((b - a) * (int64_t)sizeof(XferDesc), &dptr);
-        if (!h) return cuda_fail(cudaErrorMemoryAllocation, "descriptor ring");
-        XferDesc *hd = reinterpret_cast<XferDesc *>(h);
-        for (int64_t i = a; i < b; ++i) {
-            hd[i - a] = (*j.desc)[i];
-            hd[i - a].ext = reinterpret_cast<uint64_t>(base + (i - a) * B);
-        }
-        if ((s0 = span_begin(j.sk, &t0)) != TC_OK) return s0;
-        TC_CUDA(launch_xfer(j.gather, reinterpret_cast<const XferDesc *>(dptr), b - a, g, kv, table_dev, ctas[2],
-                            nthreads[2], variant[2], j.sk),
-                j.gather ? "gather kernel" : "scatter kernel");
+// Launches the gather/scatter of n descriptors (by value in the kernel parameters, at most kMaxInlineDesc per
+// launch) with path's launch configuration; `kind` names the timing slot (0 offload, 1 upload, 2 device tier).
+tc_status Pool::launch_descs(bool gather, int32_t kind, int path, const XferDesc *d, int64_t n, cudaStream_t s) {
+    for (int64_t a = 0; a < n; a += kMaxInlineDesc) {
+        const int32_t m = (int32_t)std::min<int64_t>(kMaxInlineDesc, n - a);
+        const XferGeom g = geom(kind, m * B);
+        TC_CUDA(launch_xfer(gather, d + a, m, g, kv, table_dev, ctas[path], nthreads[path], variant[path], s),
+                gather ? "gather kernel" : "scatter kernel");
+        trace(gather ? "gather" : "scatter");
+        ++n_launch;
     }
-    ++n_launch;
+    return TC_OK;
+}
+
+// Device-side gather/scatter of pieces [a, b) against the staging slot `base`.
+tc_status Pool::xfer_kernel(XferJob &j, int64_t a, int64_t b, char *base) {
+    cd_.resize((size_t)(b - a));
+    for (int64_t i = a; i < b; ++i) {
+        cd_[i - a] = (*j.desc)[i];
+        cd_[i - a].ext = reinterpret_cast<uint64_t>(base + (i - a) * B);
+    }
+    cudaEvent_t t0;
+    tc_status st = span_begin(j.sk, &t0);
+    if (st != TC_OK) return st;
+    if ((st = launch_descs(j.gather, j.gather ? 0 : 1, 2, cd_.data(), b - a, j.sk)) != TC_OK) return st;
     return span_end(j.sk, j.gather ? 0 : 1, t0, (b - a) * B, /*link=*/false);
 }
 
 tc_status Pool::xfer_phase_a(XferJob &j) {
     if (j.n == 0) return TC_OK;
     tc_status st;
+    if (j.mode == TC_XFER_COPY) return xfer_copy2d(j);
     if (j.mode == TC_XFER_DIRECT) {
         const bool dev_tier = j.slot_of == nullptr || j.slot_of->empty();
         const int path = dev_tier ? 2 : (j.gather ? 0 : 1);
-        const XferGeom g = geom(dev_tier ? 2 : (j.gather ? 0 : 1), j.n * B);
-        char *dptr = nullptr;
-        char *h = ring_alloc(j.n * (int64_t)sizeof(XferDesc), &dptr);
-        if (!h) return cuda_fail(cudaErrorMemoryAllocation, "descriptor ring");
-        XferDesc *hd = reinterpret_cast<XferDesc *>(h);
-        for (int64_t i = 0; i < j.n; ++i) {
-            hd[i] = (*j.desc)[i];
-            if (!dev_tier) hd[i].ext = reinterpret_cast<uint64_t>(host_dev_ptr((*j.slot_of)[i]));
+        const int32_t kind = dev_tier ? 2 : (j.gather ? 0 : 1);
+        const XferDesc *d = j.desc->data();
+        if (!dev_tier) {
+            cd_.resize((size_t)j.n);
+            for (int64_t i = 0; i < j.n; ++i) {
+                cd_[i] = (*j.desc)[i];
+                cd_[i].ext = reinterpret_cast<uint64_t>(host_dev_ptr((*j.slot_of)[i]));
+            }
+            d = cd_.data();
         }
         cudaEvent_t t0;
         if ((st = span_begin(j.s, &t0)) != TC_OK) return st;
-        TC_CUDA(launch_xfer(j.gather, reinterpret_cast<const XferDesc *>(dptr), j.n, g, kv, table_dev, ctas[path],
-                            nthreads[path], variant[path], j.s),
-                "xfer kernel");
-        ++n_launch;
-        return span_end(j.s, path == 2 ? 2 : (j.gather ? 0 : 1), t0, j.n * B);
+        if ((st = launch_descs(j.gather, kind, path, d, j.n, j.s)) != TC_OK) return st;
+        return span_end(j.s, kind, t0, j.n * B);
     }
     std::vector<int32_t> done(j.ring_reuse ? j.npieces : 0, -1);
     for (int64_t p = 0; p < j.npieces; ++p) {
@@ -520,16 +599,18 @@ tc_status Pool::xfer_phase_a(XferJob &j) {
         if (j.gather) {
             if (j.ring_reuse && p >= 2) TC_CUDA(cudaStreamWaitEvent(j.sk, events[done[p - 2]], 0), "ring reuse");
             if ((st = xfer_kernel(j, a, b, base)) != TC_OK) return st;
-            if ((st = ev_rec(j.sk, &j.ev[p])) != TC_OK) return st;
             // the D2H copy of a piece is issued right after its gather, so the link starts after the small
             // head piece's gather and a handful of API calls
-            TC_CUDA(cudaStreamWaitEvent(j.s, events[j.ev[p]], 0), "gather->D2H wait");
+            if (j.sk != j.s) {
+                if ((st = ev_rec(j.sk, &j.ev[p])) != TC_OK) return st;
+                TC_CUDA(cudaStreamWaitEvent(j.s, events[j.ev[p]], 0), "gather->D2H wait");
+            }
             if ((st = xfer_copy(j, a, b, base)) != TC_OK) return st;
             if (j.ring_reuse && (st = ev_rec(j.s, &done[p])) != TC_OK) return st;
         } else {
             if (j.ring_reuse && p >= 2) TC_CUDA(cudaStreamWaitEvent(j.s, events[done[p - 2]], 0), "ring reuse");
             if ((st = xfer_copy(j, a, b, base)) != TC_OK) return st;
-            if ((st = ev_rec(j.s, &j.ev[p])) != TC_OK) return st;
+            if (j.sk != j.s && (st = ev_rec(j.s, &j.ev[p])) != TC_OK) return st;
             if (j.ring_reuse) {
                 TC_CUDA(cudaStreamWaitEvent(j.sk, events[j.ev[p]], 0), "H2D->scatter wait");
                 if ((st = xfer_kernel(j, a, b, base)) != TC_OK) return st;
@@ -551,11 +632,11 @@ tc_status Pool::xfer_phase_b(XferJob &j) {
             TC_CUDA(cudaStreamWaitEvent(j.s, events[j.ev[p]], 0), "gather->D2H wait");
             if ((st = xfer_copy(j, a, b, base)) != TC_OK) return st;
         } else {
-            TC_CUDA(cudaStreamWaitEvent(j.sk, events[j.ev[p]], 0), "H2D->scatter wait");
+            if (j.sk != j.s) TC_CUDA(cudaStreamWaitEvent(j.sk, events[j.ev[p]], 0), "H2D->scatter wait");
             if ((st = xfer_kernel(j, a, b, base)) != TC_OK) return st;
         }
     }
-    if (!j.gather) {                                   // the upload completes when its last scatter has
+    if (!j.gather && j.sk != j.s) {                   // the upload completes when its last scatter has
         int32_t last;
         if ((st = ev_rec(j.sk, &last)) != TC_OK) return st;
         TC_CUDA(cudaStreamWaitEvent(j.s, events[last], 0), "scatter->upload join");
@@ -869,11 +950,16 @@ tc_status Pool::cycle(int32_t nh, const tc_handle *hs, const int64_t *up_off, in
                       const int32_t *ags, const int64_t *off_off, const int32_t *ids, tc_handle *out_h) {
     if (cuda_dead) return TC_E_CUDA;
     if (nh < 0 || na < 0 || (nh > 0 && !out_ids) || (na > 0 && !out_h)) return TC_E_INVAL;
+    if (g_trace) {
+        g_trace_t0 = std::chrono::steady_clock::now();
+        g_trace_buf = "[tc trace] cycle";
+    }
     UpPlan U;
     OffPlan O;
     tc_status st;
     if (nh > 0 && (st = plan_upload(U, nh, hs, up_off)) != TC_OK) return st;
     if (na > 0 && (st = plan_offload(O, na, ags, off_off, ids)) != TC_OK) return st;
+    trace("plans");
     int32_t ev_up = -1, ev_off = -1;
     if (!meta_only) {
         XferJob ju, jo;
@@ -896,6 +982,10 @@ tc_status Pool::cycle(int32_t nh, const tc_handle *hs, const int64_t *up_off, in
     }
     if (nh > 0) commit_upload(U, ev_up, out_ids);
     if (na > 0) commit_offload(O, ev_off, out_h);
+    if (g_trace) {
+        trace("commit");
+        std::fprintf(stderr, "%s\n", g_trace_buf.c_str());
+    }
     return TC_OK;
 }
 

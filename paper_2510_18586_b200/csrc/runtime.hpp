@@ -89,7 +89,7 @@ struct Pool {
     cudaStream_t s_up = nullptr, s_off = nullptr, s_compute = nullptr;
     cudaStream_t s_up_k = nullptr, s_off_k = nullptr;   // staged mode: device-side kernels of each direction
     int64_t piece_bytes = 256ll << 20;                  // staged pipeline: large pieces
-    int64_t head_bytes = 4ll << 20;                     // ... and the small head (offload) / tail (upload) piece
+    int64_t head_bytes = 0;                             // > 0: a small first (offload) / last (upload) piece
     bool use_batch_memcpy = true;
     cudaEvent_t ev_compute = nullptr;
     std::vector<cudaStream_t> foreign;       // caller streams used by the device tier
@@ -123,7 +123,7 @@ struct Pool {
         int64_t bytes;
         bool link;                           // host-link side of a transfer (DMA or direct kernel)
     };
-    bool timing = false;
+    int32_t timing = 0;                      // 0 off, 1 event spans + kernel timestamps, 2 kernel timestamps
     std::vector<Span> spans;
     std::vector<cudaEvent_t> tev_free;
     tc_timing_t tacc{};
@@ -230,6 +230,11 @@ struct Pool {
     tc_status xfer_phase_b(XferJob &j);
     tc_status xfer_copy(XferJob &j, int64_t a, int64_t b, char *base);
     tc_status xfer_kernel(XferJob &j, int64_t a, int64_t b, char *base);
+    tc_status xfer_copy2d(XferJob &j);
+    std::vector<cudaMemcpy3DBatchOp> ops_;   // scratch: COPY-mode DMA descriptors
+    int32_t auto_mode(int dir) const;
+    tc_status launch_descs(bool gather, int32_t kind, int path, const XferDesc *d, int64_t n, cudaStream_t s);
+    std::vector<XferDesc> cd_;               // scratch: descriptors of the launch being built
     tc_status ev_rec(cudaStream_t st, int32_t *out);
     std::vector<void *> cp_dst, cp_src;
     std::vector<size_t> cp_size;

@@ -24,7 +24,10 @@ from workloads.scripts import N_CLASSES, build_script, c1_worked_example, fuzz_s
 
 MODES = {"direct": (tcb.XFER_DIRECT, tcb.XFER_DIRECT, 0), "staged": (tcb.XFER_STAGED, tcb.XFER_STAGED, 0),
          "mixed": (tcb.XFER_DIRECT, tcb.XFER_STAGED, 0), "direct_tma": (tcb.XFER_DIRECT, tcb.XFER_DIRECT, 1),
-         "staged_tma": (tcb.XFER_STAGED, tcb.XFER_STAGED, 1)}
+         "staged_tma": (tcb.XFER_STAGED, tcb.XFER_STAGED, 1), "direct_tile": (tcb.XFER_DIRECT, tcb.XFER_DIRECT, 2),
+         "staged_tile": (tcb.XFER_STAGED, tcb.XFER_STAGED, 2), "staged_tma4": (tcb.XFER_STAGED, tcb.XFER_STAGED, 3),
+         "mixed_rev": (tcb.XFER_STAGED, tcb.XFER_DIRECT, 2), "copy": (tcb.XFER_COPY, tcb.XFER_COPY, 0),
+         "copy_staged": (tcb.XFER_COPY, tcb.XFER_STAGED, 3), "staged_copy": (tcb.XFER_STAGED, tcb.XFER_COPY, 3)}
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -120,10 +123,11 @@ def test_fill_kernel_matches_generator_sharded():
             c.close()
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
 def test_device_tier_equals_numpy_take(variant):
     L, H, D, N = 4, 4, 128, 64
-    c = dev_pool(L, H, D, N, 4, seed=9, mode="direct_tma" if variant else "direct")
+    c = dev_pool(L, H, D, N, 4, seed=9, mode="direct")
+    c.set_launch_config(2, 0, 256, variant)
     pool0 = content.pool_bytes(9, L, N, 16, H, D)
     rng = np.random.default_rng(0)
     ids = rng.choice(N, size=23, replace=False).astype(np.int32)
@@ -210,10 +214,10 @@ def test_full_size_config_parity(name, world):
     c.close()
 
 
-@pytest.mark.parametrize("head_kib,piece_kib", [(1, 2), (3, 1024), (64, 64)])
+@pytest.mark.parametrize("head_kib,piece_kib", [(0, 2), (1, 2), (3, 1024), (64, 64), (4096, 1024)])
 def test_staged_piece_plans_bytes(monkeypatch, head_kib, piece_kib):
-    """Staged pipelining with several pieces per batch: small head/tail pieces, multi-block pieces, and pieces above
-    the inline-descriptor limit (descriptors from the pinned ring); B = 1 KiB blocks."""
+    """Staged pipelining with several pieces per batch: small head/tail pieces, multi-block pieces, a head covering
+    the whole batch, and batches above one launch's by-value descriptor capacity; B = 1 KiB blocks."""
     monkeypatch.setenv("TC_HEAD_KIB", str(head_kib))
     monkeypatch.setenv("TC_PIECE_KIB", str(piece_kib))
     L, H, D, T, N, S = 1, 1, 64, 4, 600, 400
@@ -236,3 +240,27 @@ def test_unbuffered_ablation_bytes():
         assert a == b, (i, op, a, b)
     c.sync()
     assert np.array_equal(c.kv_tensor().cpu().numpy(), o.store.pool)
+
+
+@pytest.mark.parametrize("mode", ["direct", "staged", "staged_tile", "direct_tma", "copy"])
+def test_batches_above_one_launch_capacity(monkeypatch, mode):
+    """A batch of more blocks than one launch's by-value descriptor capacity (2040) is split over several launches:
+    offload + upload of 4100 blocks (and a device-tier gather of 4100) against the oracle / numpy."""
+    monkeypatch.setenv("TC_PIECE_KIB", "64")        # staged: 2048-block pieces, each above one launch's capacity
+    L, H, D, T, N, S = 1, 1, 8, 2, 5000, 4200
+    ops = [("agent_add", 0, 0), ("alloc", 0, 4100), ("offload", 0, "all"), ("sync",), ("upload", 0), ("sync",)]
+    pool0 = content.pool_bytes(3, L, N, T, H, D)
+    o = OraclePool(N, S, max_blocks_per_agent=8192, store=BytesStore(pool0, S))
+    c = dev_pool(L, H, D, N, S, mode, max_bpa=8192, seed=3, T=T)
+    ro, rc = Replayer(o), Replayer(c)
+    for op in ops:
+        a, b = ro.step(op), rc.step(op)
+        assert a == b and a[0] == 0, op
+    c.sync()
+    compare_full(o, c, "after 4100-block round trip")
+    ids = np.random.default_rng(1).choice(N, size=4100, replace=False).astype(np.int32)
+    dst = torch.empty(4100 * c.block_bytes, dtype=torch.uint8, device="cuda:0")
+    c.gather_dev(ids, dst.data_ptr())
+    torch.cuda.synchronize()
+    exp = np.take(o.store.pool, ids, axis=2).transpose(2, 0, 1, 3)
+    assert np.array_equal(dst.cpu().numpy().reshape(exp.shape), exp)

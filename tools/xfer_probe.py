@@ -59,14 +59,15 @@ def main():
         return agg, float(np.median([w for _, w in out])) * 1e3
 
     cfgs = []
-    for var in (0, 1):
-        for ctas in ((16, 32, 64, 148, 296, 592) if var == 0 else (16, 32, 64, 148)):
+    grids = {0: (64, 148, 296, 592), 1: (32, 64, 148), 2: (148, 296, 592, 1184), 3: (64, 148, 296)}
+    for var in (0, 1, 2, 3):
+        for ctas in grids[var]:
             cfgs.append(("direct", var, ctas))
     cfgs.append(("staged", 0, 0))
     for conc in (False, True):
         for mode, var, ctas in cfgs:
             m = tcb.XFER_DIRECT if mode == "direct" else tcb.XFER_STAGED
-            cfg = {0: (ctas, 256, var), 1: (ctas, 256, var), 2: (0, 256, 0)}
+            cfg = {0: (ctas, 256, var), 1: (ctas, 256, var), 2: (0, 256, 3)}
             try:
                 agg, wall = run(m, cfg, conc)
             except tcb.TcError as e:
