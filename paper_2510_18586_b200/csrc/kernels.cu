@@ -19,6 +19,7 @@
 // Work is split over CTAs at piece/tile granularity (variants 1-3), so a small launch (the staged head/tail piece)
 // still reaches every SM and a large one has no chunk-granular tail.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -29,6 +30,15 @@ constexpr int kUnroll = 8;
 constexpr int kTileU = 8;
 constexpr int64_t kTileBytes = kTileU * 512;   // one warp-iteration: 32 lanes x kTileU 16-byte vectors
 constexpr int64_t kPieceMax = 16384;           // TMA bulk piece (bytes per cp.async.bulk)
+
+// TMA ring bytes per CTA, overridable for tuning (TC_TMA_RING_KIB); 0 = by variant.
+inline int64_t tma_ring_override() {
+    static const int64_t v = [] {
+        const char *e = std::getenv("TC_TMA_RING_KIB");
+        return e ? std::atoll(e) * 1024 : 0ll;
+    }();
+    return v;
+}
 
 template <int kCap>
 struct Descs {
@@ -187,55 +197,80 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-template <bool kGather, int kStages>
+// Position of a piece inside the launch: block i, chunk lk of the block, piece q of the chunk.  Advanced one piece at
+// a time, so the issuing thread does no 64-bit division in its loop.
+struct Cursor {
+    int64_t i;
+    int32_t lk, q;
+    __device__ __forceinline__ void init(int64_t k, int32_t ppc, int32_t two_l) {
+        const int64_t ppb = (int64_t)ppc * two_l;
+        i = k / ppb;
+        const int32_t r = (int32_t)(k - i * ppb);
+        lk = r / ppc;
+        q = r - lk * ppc;
+    }
+    __device__ __forceinline__ void next(int32_t ppc, int32_t two_l) {
+        if (++q == ppc) {
+            q = 0;
+            if (++lk == two_l) {
+                lk = 0;
+                ++i;
+            }
+        }
+    }
+};
+
+constexpr int kMaxStages = 32;
+
+template <bool kGather>
 __device__ __forceinline__ void bulk_body(const XferDesc *__restrict__ desc, int64_t n, const XferGeom &g,
                                           char *__restrict__ kv, int32_t *__restrict__ table, int64_t per_cta,
-                                          int32_t piece, unsigned char *smem) {
-    const int64_t ppc = (g.chunk + piece - 1) / piece;   // pieces per chunk
-    const int64_t ppb = ppc * g.two_l;                   // pieces per block
-    const int64_t K = n * ppb;
+                                          int32_t piece, int32_t stages, unsigned char *smem) {
+    const int32_t ppc = (int32_t)((g.chunk + piece - 1) / piece);   // pieces per chunk
+    const int64_t K = n * ppc * g.two_l;
     const int64_t k0 = (int64_t)blockIdx.x * per_cta;
     if (k0 >= K || threadIdx.x != 0) return;
-    const int64_t k1 = min(K, k0 + per_cta);
-    unsigned char *ring = smem;                                                       // kStages x piece
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + (size_t)kStages * piece);  // kStages mbarriers
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    const int64_t total = min(K, k0 + per_cta) - k0;
+    unsigned char *ring = smem;                                                      // stages x piece
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + (size_t)stages * piece);  // stages mbarriers
+    for (int s = 0; s < stages; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     ts_begin(g);
-    // piece k -> (src, dst, bytes); the load of a block's first piece carries the table epilogue
-    auto where = [&](int64_t k, char *&src, char *&dst, uint32_t &bytes, bool epi) {
-        const int64_t i = k / ppb;
-        const int64_t r = k - i * ppb;
-        const int64_t lk = r / ppc;
-        const int64_t off = (r - lk * ppc) * piece;
-        const XferDesc d = desc[i];
-        const Loc p = locate(d, lk, off, g, kv);
-        bytes = (uint32_t)min((int64_t)piece, g.chunk - off);
-        src = kGather ? p.pool : p.ext;
-        dst = kGather ? p.ext : p.pool;
-        if (epi && r == 0 && d.tab >= 0) table[d.tab] = kGather ? -1 : d.blk;
+    Cursor ld, st;
+    ld.init(k0, ppc, g.two_l);
+    st = ld;
+    int sl = 0, ss = 0;
+    uint32_t phase = 0;
+    int64_t issued = 0;
+    // load of the next piece into stage sl; the load of a block's first piece carries the table epilogue
+    auto issue_load = [&]() {
+        const XferDesc d = desc[ld.i];
+        const int64_t off = (int64_t)ld.q * piece;
+        const Loc p = locate(d, ld.lk, off, g, kv);
+        const uint32_t bytes = (uint32_t)min((int64_t)piece, g.chunk - off);
+        if (ld.lk == 0 && ld.q == 0 && d.tab >= 0) table[d.tab] = kGather ? -1 : d.blk;
+        mbar_expect_tx(&bars[sl], bytes);
+        bulk_load(ring + (size_t)sl * piece, kGather ? p.pool : p.ext, bytes, &bars[sl]);
+        ld.next(ppc, g.two_l);
+        if (++sl == stages) sl = 0;
+        ++issued;
     };
-    auto issue_load = [&](int64_t k) {
-        char *src, *dst;
-        uint32_t bytes;
-        where(k, src, dst, bytes, true);
-        const int s = (int)((k - k0) % kStages);
-        mbar_expect_tx(&bars[s], bytes);
-        bulk_load(ring + (size_t)s * piece, src, bytes, &bars[s]);
-    };
-    for (int64_t k = k0; k < k1 && k < k0 + kStages; ++k) issue_load(k);
-    for (int64_t k = k0; k < k1; ++k) {
-        const int64_t q = k - k0;
-        const int s = (int)(q % kStages);
-        mbar_wait(&bars[s], (uint32_t)((q / kStages) & 1));
-        char *src, *dst;
-        uint32_t bytes;
-        where(k, src, dst, bytes, false);
-        bulk_store(dst, ring + (size_t)s * piece, bytes);
+    while (issued < total && issued < stages) issue_load();
+    for (int64_t q = 0; q < total; ++q) {
+        mbar_wait(&bars[ss], phase);
+        const XferDesc d = desc[st.i];
+        const int64_t off = (int64_t)st.q * piece;
+        const Loc p = locate(d, st.lk, off, g, kv);
+        bulk_store(kGather ? p.ext : p.pool, ring + (size_t)ss * piece, (uint32_t)min((int64_t)piece, g.chunk - off));
         bulk_commit();
-        if (q >= 1 && k - 1 + kStages < k1) {   // refill the previous stage once its store has read smem
+        st.next(ppc, g.two_l);
+        if (q >= 1 && issued < total) {   // refill the stage the previous store drained, once it has read smem
             bulk_wait_read1();
-            issue_load(k - 1 + kStages);
+            issue_load();
+        }
+        if (++ss == stages) {
+            ss = 0;
+            phase ^= 1;
         }
     }
     bulk_wait_all();
@@ -257,12 +292,12 @@ __global__ void __launch_bounds__(256) k_xfer_tile(const __grid_constant__ Descs
     tile_body<kGather>(dd.d, n, g, kv, table, per_cta);
 }
 
-template <bool kGather, int kStages, int kCap>
+template <bool kGather, int kCap>
 __global__ void __launch_bounds__(32) k_xfer_bulk(const __grid_constant__ Descs<kCap> dd, int32_t n, XferGeom g,
                                                   char *__restrict__ kv, int32_t *__restrict__ table,
-                                                  int64_t per_cta, int32_t piece) {
+                                                  int64_t per_cta, int32_t piece, int32_t stages) {
     extern __shared__ __align__(128) unsigned char smem[];
-    bulk_body<kGather, kStages>(dd.d, n, g, kv, table, per_cta, piece, smem);
+    bulk_body<kGather>(dd.d, n, g, kv, table, per_cta, piece, stages, smem);
 }
 
 // Even split of `units` work units over at most `ctas` CTAs (each >= `min_per_cta` units): {grid, units per CTA}.
@@ -279,16 +314,20 @@ cudaError_t launch_cap(bool gather, const XferDesc *host_desc, int32_t n, const 
     std::copy(host_desc, host_desc + n, dd.d);
     int64_t grid = 0, per = 0;
     if (variant == 1 || variant == 3) {
+        // ring bytes per CTA: 128 KiB, one CTA per SM (1) / 96 KiB, two resident per SM over a 3-per-SM grid, i.e.
+        // 1.5 waves that even out per-channel speed differences (3; profiles/r01_tier_probe_c5_v3.log: 0.98 of the
+        // HBM copy peak at 512 MiB for both 16 KiB and 4 KiB chunks).  stages = ring / piece, so small chunks keep as
+        // many bytes in flight as large ones.
         const int32_t piece = (int32_t)std::min<int64_t>(g.chunk, kPieceMax);
         const int64_t K = (int64_t)n * g.two_l * ((g.chunk + piece - 1) / piece);
-        const int stages = variant == 1 ? 8 : 4;
-        split(K, ctas > 0 ? ctas : (variant == 1 ? 148 : 296), 1, &grid, &per);
+        const int64_t ring = tma_ring_override() > 0 ? tma_ring_override() : (variant == 1 ? 128 << 10 : 96 << 10);
+        const int32_t stages = (int32_t)std::max<int64_t>(2, std::min<int64_t>(kMaxStages, ring / piece));
+        split(K, ctas > 0 ? ctas : (variant == 1 ? 148 : 444), 1, &grid, &per);
         const size_t smem = (size_t)stages * piece + stages * sizeof(uint64_t);
-        auto fn = variant == 1 ? (gather ? k_xfer_bulk<true, 8, kCap> : k_xfer_bulk<false, 8, kCap>)
-                               : (gather ? k_xfer_bulk<true, 4, kCap> : k_xfer_bulk<false, 4, kCap>);
+        auto fn = gather ? k_xfer_bulk<true, kCap> : k_xfer_bulk<false, kCap>;
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        fn<<<(unsigned)grid, 32, smem, s>>>(dd, n, g, kv, table, per, piece);
+        fn<<<(unsigned)grid, 32, smem, s>>>(dd, n, g, kv, table, per, piece, stages);
         return cudaGetLastError();
     }
     if (threads <= 0 || threads > 256) threads = 256;

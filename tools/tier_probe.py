@@ -28,7 +28,10 @@ def main():
     rng = np.random.default_rng(7)
     sizes_mib = [int(x) for x in os.environ.get("PSIZES", "1,4,32,104,512").split(",")]
     variants = [int(x) for x in os.environ.get("PVARS", "0,1,2,3").split(",")]
-    grids = {0: [0, 1184], 1: [0, 296], 2: [0, 888, 1184, 2368], 3: [0, 444, 592]}
+    grids = {0: [0], 1: [0, 296], 2: [0, 1184, 2368], 3: [0, 444, 592]}
+    if os.environ.get("PGRIDS"):
+        grids = json.loads(os.environ["PGRIDS"])
+        grids = {int(k): v for k, v in grids.items()}
     dst = torch.empty((max(sizes_mib) << 20) + B, dtype=torch.uint8, device=dev)
     res = []
     for mib in sizes_mib:
