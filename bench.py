@@ -344,6 +344,7 @@ def run_ours(args):
                 "unit": "GB/s", "frac": kd["frac"], "traffic": None, "bytes_per_launch": kd["bytes_per_launch"],
                 "ms_per_launch": kd["ms_per_launch"], "peak_source": kd["peak_source"],
                 "share_of_kernel_time": kd["ms_total"] / sum(v["ms_total"] for v in kern_only.values())}
+        roof.update(ncu_traffic(cfg.name, "gather" if dom == "offload_kernel" else "scatter", kd))
     # the step's binding resource is the host link: per-direction DMA/kernel rate and a per-step link roofline
     link_roof = None
     if link:
@@ -395,6 +396,24 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier(); dist.destroy_process_group()
+
+
+def ncu_traffic(cfg_name, kind, kd):
+    """roofline.traffic for the staged HBM kernels: DRAM bytes per launch from the committed `ncu --set full` capture
+    of fixed-size launches of the same kernel on the same config (tools/traffic_probe.py -> profiles/
+    r01_traffic_<cfg>.json), as the captured ratio (dram read + write) / algorithmic bytes times this run's per-launch
+    algorithmic bytes.  None when no capture exists or the kernel is a host-link one."""
+    path = os.path.join(ROOT, "profiles", f"r01_traffic_{cfg_name}.json")
+    if kd.get("bound") != "hbm" or not os.path.exists(path):
+        return {}
+    cap = [x for x in json.load(open(path))["launches"] if x["kind"] == kind]
+    if not cap:
+        return {}
+    ratio = statistics.mean(x["ratio"] for x in cap)
+    return {"traffic": ratio * kd["bytes_per_launch"],
+            "traffic_source": {"capture": os.path.relpath(path, ROOT), "dram_over_algorithmic": ratio,
+                               "dram_read_over_algorithmic_read": statistics.mean(x["read_ratio"] for x in cap),
+                               "note": "ncu counts writes still dirty in L2 at kernel end as not yet written"}}
 
 
 def timeline_summary(spans):
