@@ -13,8 +13,8 @@ class Fail(Exception):
 
 
 class SetModel:
-    def __init__(self, N, S, ncls=2):
-        self.N, self.S = N, S
+    def __init__(self, N, S, ncls=2, P=0):
+        self.N, self.S, self.P = N, S, P
         self.free = set(range(N))
         self.pend = []                   # list of (cls, frozenset ids)
         self.own = {}                    # id -> (agent, pos)
@@ -23,6 +23,7 @@ class SetModel:
         self.res = [0] * ncls
         self.clm = [0] * ncls
         self.stack = list(range(S))[::-1]
+        self.pstack = list(range(S, S + P))[::-1]    # peer-tier slots (NEXT-2), ids after the host slots
         self.back = []
         self.live = {}                   # handle -> (agent, cls, pos list, slot list)
         self.dead = set()
@@ -61,12 +62,14 @@ class SetModel:
     def offload(self, a, ids):
         if not ids or len(set(ids)) < len(ids) or any(self.own.get(b, (None,))[0] != a for b in ids):
             raise Fail(INVAL)
-        if len(self.stack) < len(ids):
+        # whole offload to the peer tier if it fits there, else to the host tier, else refused
+        tier = self.pstack if len(self.pstack) >= len(ids) else self.stack
+        if len(tier) < len(ids):
             raise Fail(NOHOST)
         slots = []
         pos = []
         for b in ids:
-            s = self.stack.pop()
+            s = tier.pop()
             slots.append(s)
             self.hprov[s] = self.prov[b]
             p = self.own.pop(b)[1]
@@ -131,7 +134,8 @@ class SetModel:
             self.free |= ids
             self.clm[c] = max(0, self.clm[c] - len(ids))
         self.pend = []
-        self.stack += self.back
+        self.stack += [s for s in self.back if s < self.S]
+        self.pstack += [s for s in self.back if s >= self.S]
         self.back = []
 
     def agent_free(self, a):

@@ -91,7 +91,7 @@ def compare(p: OraclePool, m: SetModel, pool0, where):
         {h: v for h, v in m.rsv.items() if v}, where
     assert p.block_table(A) == m.tab[A] and p.block_table(B) == m.tab[B], where
     assert p.reserved == m.res and p.claimed == m.clm, where
-    assert p.slot_free == m.stack and p.released_slots == m.back, where
+    assert p.slot_free == m.stack and p.released_slots == m.back and p.peer_free == m.pstack, where
     live = {h: (x.agent, x.pos, x.slots) for h, x in p.handles.items() if x.state == OFFLOADED}
     assert live == {h: (v[0], v[2], v[3]) for h, v in m.live.items()}, where
     # payload: every physical block holds the original bytes of the model's provenance; live slots likewise
@@ -105,19 +105,20 @@ def compare(p: OraclePool, m: SetModel, pool0, where):
 def key(p: OraclePool, m: SetModel):
     return (p.blk_state.tobytes(), p.owner.tobytes(), p.store.pool.tobytes(), p.store.host.tobytes(),
             tuple(tuple(g.table) for g in p.agents.values()), tuple(p.reserved), tuple(p.claimed),
-            tuple(p.slot_free), tuple(p.released_slots), tuple(map(tuple, (x[1] for x in p.pending_dev))),
+            tuple(p.slot_free), tuple(p.peer_free), tuple(p.released_slots),
+            tuple(map(tuple, (x[1] for x in p.pending_dev))),
             tuple((h, x.state, tuple(x.pos), tuple(x.slots)) for h, x in p.handles.items()), p.next_handle,
             tuple(sorted(m.free)), tuple(sorted(m.prov.items())), tuple(sorted(m.hprov.items())),
-            tuple(m.stack), tuple(m.back), tuple(sorted(m.live)),
+            tuple(m.stack), tuple(m.pstack), tuple(m.back), tuple(sorted(m.live)),
             tuple((h, tuple(x.plan), x.ticks, tuple(x.resv)) for h, x in p.handles.items()),
             tuple(sorted((h, tuple(v[0]), v[1]) for h, v in m.rplan.items())),
             tuple(sorted((h, tuple(v)) for h, v in m.rsv.items())))
 
 
-def explore(N, S, depth, alphabet=ALPHABET):
+def explore(N, S, depth, alphabet=ALPHABET, P=0):
     pool0 = content.pool_bytes(9, 1, N, 1, 1, 8)          # C = 16 bytes per chunk
-    p = OraclePool(N, S, n_classes=2, store=BytesStore(pool0, S))
-    m = SetModel(N, S)
+    p = OraclePool(N, S, n_classes=2, store=BytesStore(pool0, S + P), n_peer_slots=P)
+    m = SetModel(N, S, P=P)
     for a, c in ((A, 0), (B, 1)):
         p.agent_add(a, c)
         m.add(a, c)
@@ -188,3 +189,11 @@ def test_c1_offload_all_subsets_both_orders():
             for q, b in zip(pos, new):
                 assert t2[q] == b
             assert all(t2[i] == tab[i] for i in range(8) if i not in pos)
+
+
+@pytest.mark.parametrize("N,S,P,depth", [(4, 2, 1, 5), (5, 2, 2, 5), (6, 3, 2, 5)])
+def test_bruteforce_peer_tier(N, S, P, depth):
+    """NEXT-2 peer tier (reading C1): offloads land in the peer slots when the whole offload fits, else in the
+    host buffer, else NOHOST; slots return to their own tier at sync."""
+    nodes, states = explore(N, S, depth, P=P)
+    assert nodes > 1000 and states > 100

@@ -269,3 +269,57 @@ def test_gradual_reservation_shortfall_carries_and_cancel():
     after = p.stats()
     assert after["free"] == before["free"] + 8 and after["reserved_blocks"] == 0
     assert p.upload(h) == list(range(12))             # plain lowest-free upload after the cancel
+
+
+def test_next2_peer_tier_worked_example():
+    """NEXT-2 peer tier (reading C1) — tests/golden/next2_peer_tier.json, hand-derived."""
+    g = gold("next2_peer_tier.json")
+    N, S, P = g["N"], g["S"], g["P"]
+    pool0 = content.pool_bytes(5, 2, N, 16, 1, 8)
+    p = OraclePool(N, S, store=BytesStore(pool0, S + P), n_peer_slots=P)
+    p.agent_add(0, 0)
+    p.agent_add(1, 1)
+    codes = {"NOHOST": E_NOHOST}
+    for st in g["steps"]:
+        if st["op"] == "alloc":
+            assert p.alloc(st["agent"], st["n"]) == st["expect"]
+        elif st["op"] == "offload":
+            if "expect_status" in st:
+                before = full_state(p)
+                assert status_of(p.offload, st["agent"], st["ids"]) == codes[st["expect_status"]]
+                assert same(before, full_state(p))
+                continue
+            h = p.offload(st["agent"], st["ids"])
+            assert p.handles[h].slots == st["expect_slots"], st
+        elif st["op"] == "upload":
+            assert p.upload(st["handle"]) == st["expect"]
+        elif st["op"] == "sync":
+            p.sync()
+            assert p.stats()["free"] == st["expect_free_blocks"]
+        s = p.stats()
+        if "expect_peer_free" in st:
+            assert s["peer_free"] == st["expect_peer_free"] and s["host_free"] == st["expect_host_free"], st
+    for new, orig in zip((13, 14, 15), (0, 1, 2)):
+        assert np.array_equal(p.store.pool[:, :, new], pool0[:, :, orig])
+    s = p.stats()
+    assert s["peer_used"] == 4 and s["host_used"] == 6          # peer: handle 3 (slot 11) + the last offload
+
+
+def test_peer_tier_slot_conservation():
+    """With P = 0 the peer tier never engages (every slot id < S); with P > 0 a random script conserves slots per
+    tier after every op (per tier)."""
+    from workloads.scripts import fuzz_script
+    N, S = 40, 12
+    for P in (0, 6):
+        pool0 = content.pool_bytes(11, 2, N, 16, 1, 8)
+        p = OraclePool(N, S, n_classes=2, store=BytesStore(pool0, S + P), n_peer_slots=P)
+        r = Replayer(p)
+        for op in fuzz_script(21, n_ops=120, n_agents=3, n_classes=2, N=N, max_alloc=5):
+            r.step(op)
+            s = p.stats()
+            assert s["host_free"] + s["host_used"] + sum(1 for x in p.released_slots if x < S) == S
+            assert s["peer_free"] + s["peer_used"] + sum(1 for x in p.released_slots if x >= S) == P
+            if P == 0:
+                assert all(x < S for h in p.handles.values() for x in h.slots)
+        if P:
+            assert any(x >= S for h in p.handles.values() for x in h.slots)
