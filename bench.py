@@ -34,6 +34,7 @@ from workloads.scripts import CycleGen, setup_ops  # noqa: E402
 METRIC = "KV offload/upload GB/s and blocks/s per GPU vs host-link & HBM peak at 1/2/4/8 GPUs"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 XFER_NAMES = {1: "direct", 2: "staged", 3: "copy"}
+NVLINK_GBS = 900.0      # NVLink 5 per direction per GPU (task statement); only used when a real peer GPU exists
 HBM_FALLBACK = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback (GB/s), only if MEASURED_PEAKS.json is absent
 
 
@@ -46,6 +47,9 @@ def parse():
     ap.add_argument("--workload", default=None)
     ap.add_argument("--mode", default="auto", choices=["auto", "direct", "staged", "copy", "mixed", "mixed_rev"],
                     help="transfer path per direction; mixed = direct D2H + staged H2D, mixed_rev = the reverse")
+    ap.add_argument("--peer", action="store_true",
+                    help="NEXT-2 peer tier: as many peer slots as host slots, in the next GPU's HBM (this GPU's own "
+                         "HBM when it is alone); offloads go there first")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--quick", action="store_true", help="skip host-link probe and device-tier microbench")
@@ -174,9 +178,10 @@ def run_ours(args):
     S = cfg.host_slots()
 
     link = None if args.quick else hostlink_peak(torch, dev)
+    peer_dev = ((local + 1) % torch.cuda.device_count()) if args.peer else -1
     pool = tcb.Pool(cfg.L, cfg.H, cfg.D, cfg.T, cfg.dtype, cfg.N, device=local, shard_rank=shard_rank, shard_world=G,
                     host_slots=S, max_agents=1024, max_blocks_per_agent=cfg.max_blocks_per_agent,
-                    xfer_d2h=mode_d2h, xfer_h2d=mode_h2d)
+                    xfer_d2h=mode_d2h, xfer_h2d=mode_h2d, peer_device=peer_dev, peer_slots=S if args.peer else 0)
     pool.fill(cfg.seed)
     B = pool.block_bytes
 
@@ -308,9 +313,12 @@ def run_ours(args):
     # roofline of the dominant kernel: per-launch algorithmic bytes / the launch's device duration
     stats = pool.stats()
     link_bound = {"offload_kernel": stats["xfer_d2h"] == tcb.XFER_DIRECT,
-                  "upload_kernel": stats["xfer_h2d"] == tcb.XFER_DIRECT}
+                  "upload_kernel": stats["xfer_h2d"] == tcb.XFER_DIRECT,
+                  "offload_peer_kernel": False, "upload_peer_kernel": False}
     kern = {}
-    for k, peak_key in (("offload_kernel", "d2h_gbs"), ("upload_kernel", "h2d_gbs")):
+    self_peer = args.peer and peer_dev == local
+    for k, peak_key in (("offload_kernel", "d2h_gbs"), ("upload_kernel", "h2d_gbs"),
+                        ("offload_peer_kernel", None), ("upload_peer_kernel", None)):
         # kernel duration = first CTA start -> last CTA end on the device clock (%globaltimer), recorded by the
         # kernel itself on the stream it runs on; the CUDA-event span around the launch (which also counts host
         # launch latency when the stream was idle) is kept beside it
@@ -319,15 +327,18 @@ def run_ours(args):
             continue
         e = {"ms_total": ms, "launches": cnt, "bytes_per_launch": byt / cnt, "ms_per_launch": ms / cnt,
              "timing": "kernel-recorded %globaltimer first-CTA start -> last-CTA end, every launch of the timed region"}
-        if link_bound[k]:      # mapped-host kernel: every byte crosses the host link once
+        if "peer" in k and not self_peer:   # neighbour's HBM over NVLink: B per block over the link
+            e.update(bound="nvlink", achieved=byt / (ms * 1e-3) / 1e9, peak=NVLINK_GBS,
+                     peak_source="NVLink 5 nominal per direction (no measured peak in MEASURED_PEAKS.json)")
+        elif "peer" in k or not link_bound[k]:   # device-side kernel (staged, or a same-GPU peer slab): HBM r+w
+            e.update(bound="hbm", achieved=2 * byt / (ms * 1e-3) / 1e9, peak=hbm, peak_source=hbm_src,
+                     bytes_per_launch=2 * byt / cnt)
+        else:                  # mapped-host kernel: every byte crosses the host link once
             pk = link[peak_key] if link else None
             e.update(bound="host_link", achieved=byt / (ms * 1e-3) / 1e9, peak=pk,
                      peak_source="live pinned cudaMemcpyAsync 1 GiB in this run (" + peak_key + ")")
             if link:
                 e["frac_of_bidir_share"] = e["achieved"] / (link["bidir_gbs"] / 2)
-        else:                  # staged device-side gather/scatter: HBM read + write of every byte
-            e.update(bound="hbm", achieved=2 * byt / (ms * 1e-3) / 1e9, peak=hbm, peak_source=hbm_src,
-                     bytes_per_launch=2 * byt / cnt)
         e["frac"] = e["achieved"] / e["peak"] if e["peak"] else None
         kern[k] = e
     for k in ("memcpy_d2h", "memcpy_h2d"):
@@ -344,10 +355,11 @@ def run_ours(args):
                 "unit": "GB/s", "frac": kd["frac"], "traffic": None, "bytes_per_launch": kd["bytes_per_launch"],
                 "ms_per_launch": kd["ms_per_launch"], "peak_source": kd["peak_source"],
                 "share_of_kernel_time": kd["ms_total"] / sum(v["ms_total"] for v in kern_only.values())}
-        roof.update(ncu_traffic(cfg.name, "gather" if dom == "offload_kernel" else "scatter", kd))
+        if "peer" not in dom:
+            roof.update(ncu_traffic(cfg.name, "gather" if dom.startswith("offload") else "scatter", kd))
     # the step's binding resource is the host link: per-direction DMA/kernel rate and a per-step link roofline
     link_roof = None
-    if link:
+    if link and not args.peer:
         bi = link["bidir_gbs"] / 2
         tmin = 0.0
         for u, o in step_bytes:
@@ -375,7 +387,10 @@ def run_ours(args):
                    "host_slots": S, "agents": cfg.n_agents, "per_cycle": cfg.per_cycle,
                    "xfer": XFER_NAMES[stats["xfer_d2h"]] + "/" + XFER_NAMES[stats["xfer_h2d"]],
                    "l2": "flushed between steps (256 MiB write, outside the step events)",
-                   "parallelism": f"{world} independent ranks" + (f", head-sharded G={G}" if G > 1 else "")},
+                   "parallelism": f"{world} independent ranks" + (f", head-sharded G={G}" if G > 1 else ""),
+                   "offload_tier": ("peer slots on GPU %d (%s) first, then host" % (
+                       peer_dev, "this GPU's own HBM" if peer_dev == local else "NVLink neighbour")) if args.peer
+                   else "host"},
         "blocks_per_s": all_blocks / (dev_total_ms * 1e-3),
         "bytes_per_step": all_bytes / n_steps,
         "gpu_launches": int(launches),

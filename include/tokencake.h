@@ -84,6 +84,14 @@ typedef struct tc_pool_desc {
     int32_t unbuffered;          /* ABLATION ONLY (Fig. 11): no CPU block buffer — each offload
                                     cudaHostAlloc's its own pinned memory, freed (cudaFreeHost) when its upload
                                     retires; the bursty host allocation pattern of P:470-479.  0 = normal. */
+    /* NEXT-2 peer tier ("a neighboring GPU's memory over high-speed interconnects like NVLink as a
+       faster offload target than CPU RAM"; reading C1).  peer_slots > 0 block-shard slots are allocated
+       in peer_device's HBM (peer access enabled; peer_device == device is allowed: an HBM-resident tier).  An
+       offload goes whole to the peer tier when its free list holds all the blocks, else whole to the host buffer,
+       else TC_E_NOHOST.  Peer slots are moved by the device-side gather/scatter kernel writing/reading the peer's
+       memory directly (launch path 3).  Incompatible with `unbuffered` (TC_E_INVAL).  Defaults: -1 / 0 = none. */
+    int32_t peer_device;
+    int64_t peer_slots;
 } tc_pool_desc;
 
 typedef struct tc_stats_t {
@@ -97,6 +105,7 @@ typedef struct tc_stats_t {
     int64_t bytes_d2h, bytes_h2d;              /* cumulative KV payload bytes enqueued */
     int32_t xfer_d2h, xfer_h2d;                /* effective modes (AUTO resolved) */
     int64_t reserved_blocks;                   /* claimed by gradual reservations, not yet uploaded into */
+    int64_t peer_slots, peer_free, peer_used;  /* NEXT-2 peer tier (0 without one) */
 } tc_stats_t;
 
 /* ---- pool lifecycle ------------------------------------------------------------------------------------------ */
@@ -117,7 +126,8 @@ tc_status tc_streams(tc_pool *p, void **upload_stream, void **offload_stream);
 /* Override the transfer mode per direction (tc_xfer_mode) for subsequent calls. */
 tc_status tc_set_xfer_mode(tc_pool *p, int32_t d2h, int32_t h2d);
 /* Launch configuration of one kernel path: path 0 = direct D2H gather, 1 = direct H2D scatter, 2 = device-side
-   gather/scatter (staged mode and device tier).  ctas <= 0 -> default grid; threads in {32..256} (SIMT variant);
+   gather/scatter (staged mode and device tier), 3 = peer-tier gather/scatter (NEXT-2).  ctas <= 0 -> default grid;
+   threads in {32..256} (SIMT variants);
    variant 0 = SIMT warp-per-chunk 16-byte copies, 1 = TMA bulk copies (cp.async.bulk through an 8-stage
    shared-memory ring, one elected thread per CTA, one CTA per SM), 2 = SIMT tile split (4 KiB warp tiles spread
    evenly over all CTAs), 3 = TMA bulk with a 4-stage ring (two CTAs per SM).  Other values -> TC_E_INVAL.
@@ -192,12 +202,17 @@ tc_status tc_block_table_dev(tc_pool *p, int32_t **dev_table, int64_t *row_strid
 tc_status tc_handle_info(tc_pool *p, tc_handle h, int32_t *agent, int64_t *n, int32_t *state);
 /* Host pointer to the pinned copy of block i of an offloaded handle, layout [L][2][C] (valid after tc_wait). */
 tc_status tc_handle_host(tc_pool *p, tc_handle h, int64_t i, const void **host_ptr);
+/* Copy block i's image ([L][2][C], B bytes) of an offloaded handle — from its host slot or its peer-tier slot — into
+   the caller's host buffer `dst` (blocking; waits for the handle's transfer).  TC_E_HANDLE if h is not offloaded,
+   TC_E_INVAL for a bad i or dst, TC_E_NODEV on a metadata-only pool.  *tier (optional) = 0 host, 1 peer. */
+tc_status tc_handle_read(tc_pool *p, tc_handle h, int64_t i, void *dst, int32_t *tier);
 tc_status tc_stats(tc_pool *p, tc_stats_t *s);
 /* Per-launch device timing (CUDA events recorded on the launching stream around every kernel / memcpy run).
    Spans complete at tc_sync, where their durations are accumulated.  Index (TC_NKINDS): 0 offload kernels (direct
    mode: the whole transfer; staged mode: the device-side gather), 1 upload kernels (likewise; scatter), 2
-   device-tier kernels, 3 D2H memcpy (staged / copy mode), 4 H2D memcpy.  bytes = KV payload bytes moved (n * B). */
-#define TC_NKINDS 5
+   device-tier kernels, 3 D2H memcpy (staged / copy mode), 4 H2D memcpy, 5 peer-tier offload kernels, 6 peer-tier
+   upload kernels.  bytes = KV payload bytes moved (n * B). */
+#define TC_NKINDS 7
 typedef struct tc_timing_t {
     double ms[TC_NKINDS];
     int64_t count[TC_NKINDS];

@@ -30,7 +30,7 @@ SYMBOLS = [
     "tc_agent_add", "tc_alloc", "tc_agent_free", "tc_offload", "tc_upload", "tc_offload_batch", "tc_upload_batch",
     "tc_cycle", "tc_reserve_begin", "tc_reserve_tick", "tc_reserve_cancel", "tc_reserve_info",
     "tc_query", "tc_wait", "tc_stream_wait", "tc_sync", "tc_block_table", "tc_block_table_dev", "tc_handle_info",
-    "tc_handle_host", "tc_stats", "tc_timing", "tc_timeline", "tc_strerror", "tc_last_error", "tc_gather_dev",
+    "tc_handle_host", "tc_handle_read", "tc_stats", "tc_timing", "tc_timeline", "tc_strerror", "tc_last_error", "tc_gather_dev",
     "tc_scatter_dev",
     # decision layers (paper_2510_18586_b200/sched.py binds them)
     "tc_fc_predict", "tc_fc_observe", "tc_transfer_ms", "tc_xfer_model_measure", "tc_should_offload",
@@ -53,14 +53,15 @@ class PoolDesc(ctypes.Structure):
         ("host_slots", ctypes.c_int64), ("n_classes", ctypes.c_int32), ("max_agents", ctypes.c_int32),
         ("max_blocks_per_agent", ctypes.c_int32), ("kv_dev", ctypes.c_void_p), ("table_dev", ctypes.c_void_p),
         ("xfer_d2h", ctypes.c_int32), ("xfer_h2d", ctypes.c_int32), ("staging_bytes", ctypes.c_int64),
-        ("desc_bytes", ctypes.c_int64), ("unbuffered", ctypes.c_int32),
+        ("desc_bytes", ctypes.c_int64), ("unbuffered", ctypes.c_int32), ("peer_device", ctypes.c_int32),
+        ("peer_slots", ctypes.c_int64),
     ]
 
 
 class Timing(ctypes.Structure):
-    _fields_ = [("ms", ctypes.c_double * 5), ("count", ctypes.c_int64 * 5), ("bytes", ctypes.c_int64 * 5),
-                ("kernel_ms", ctypes.c_double * 5), ("kernel_count", ctypes.c_int64 * 5),
-                ("kernel_bytes", ctypes.c_int64 * 5)]
+    _fields_ = [("ms", ctypes.c_double * 7), ("count", ctypes.c_int64 * 7), ("bytes", ctypes.c_int64 * 7),
+                ("kernel_ms", ctypes.c_double * 7), ("kernel_count", ctypes.c_int64 * 7),
+                ("kernel_bytes", ctypes.c_int64 * 7)]
 
 
 class Span(ctypes.Structure):
@@ -68,8 +69,9 @@ class Span(ctypes.Structure):
                 ("end_ms", ctypes.c_double), ("bytes", ctypes.c_int64)]
 
 
-TIMING_KINDS = ("offload_kernel", "upload_kernel", "device_kernel", "memcpy_d2h", "memcpy_h2d")
-KERNEL_KINDS = (0, 1, 2)
+TIMING_KINDS = ("offload_kernel", "upload_kernel", "device_kernel", "memcpy_d2h", "memcpy_h2d", "offload_peer_kernel",
+                "upload_peer_kernel")
+KERNEL_KINDS = (0, 1, 2, 5, 6)
 
 
 class Stats(ctypes.Structure):
@@ -81,7 +83,8 @@ class Stats(ctypes.Structure):
         ("reserved", ctypes.c_int64 * 64), ("claimed", ctypes.c_int64 * 64), ("live_handles", ctypes.c_int64),
         ("kernel_launches", ctypes.c_int64), ("memcpy_calls", ctypes.c_int64), ("bytes_d2h", ctypes.c_int64),
         ("bytes_h2d", ctypes.c_int64), ("xfer_d2h", ctypes.c_int32), ("xfer_h2d", ctypes.c_int32),
-        ("reserved_blocks", ctypes.c_int64),
+        ("reserved_blocks", ctypes.c_int64), ("peer_slots", ctypes.c_int64), ("peer_free", ctypes.c_int64),
+        ("peer_used", ctypes.c_int64),
     ]
 
 
@@ -123,6 +126,7 @@ def _load() -> ctypes.CDLL:
         "tc_block_table_dev": (I32, [P, ctypes.POINTER(PI32), PI64]),
         "tc_handle_info": (I32, [P, U64, PI32, PI64, PI32]),
         "tc_handle_host": (I32, [P, U64, I64, ctypes.POINTER(VP)]),
+        "tc_handle_read": (I32, [P, U64, I64, VP, PI32]),
         "tc_stats": (I32, [P, ctypes.POINTER(Stats)]),
         "tc_timing": (I32, [P, I32, ctypes.POINTER(Timing)]),
         "tc_timeline": (I32, [P, I64, ctypes.POINTER(Span), PI64]),
@@ -160,7 +164,7 @@ class Pool:
                  n_blocks: int = 64, *, device: int = 0, shard_rank: int = 0, shard_world: int = 1,
                  host_slots: int = 0, n_classes: int = 8, max_agents: int = 1024, max_blocks_per_agent: int = 4096,
                  xfer_d2h: int = XFER_AUTO, xfer_h2d: int = XFER_AUTO, staging_bytes: int = 0,
-                 torch_memory: bool = True, unbuffered: bool = False):
+                 torch_memory: bool = True, unbuffered: bool = False, peer_device: int = -1, peer_slots: int = 0):
         d = PoolDesc()
         lib.tc_pool_desc_init(ctypes.byref(d), layers, kv_heads, head_dim, block_tokens, DTYPES[dtype], n_blocks)
         d.device = device
@@ -170,6 +174,7 @@ class Pool:
         d.xfer_d2h, d.xfer_h2d = xfer_d2h, xfer_h2d
         d.staging_bytes = staging_bytes
         d.unbuffered = 1 if unbuffered else 0
+        d.peer_device, d.peer_slots = peer_device, peer_slots
         self._keep = []
         self.device = device
         self.meta_only = device < 0
@@ -354,11 +359,19 @@ class Pool:
         return a.value, n.value, s.value
 
     def handle_host_bytes(self, h: int, i: int) -> np.ndarray:
-        """Copy of the pinned host image [L][2][C] of block i of an offloaded handle (call wait() first)."""
-        p = ctypes.c_void_p()
-        self._check(lib.tc_handle_host(self._h, h, i, ctypes.byref(p)))
-        buf = (ctypes.c_uint8 * self.block_bytes).from_address(p.value)
-        return np.frombuffer(buf, dtype=np.uint8).copy().reshape(self.L, 2, self.chunk_bytes)
+        """Copy of the offloaded image [L][2][C] of block i of a handle, from its host slot or peer-tier slot
+        (tc_handle_read waits for the handle's transfer)."""
+        buf = np.empty(self.block_bytes, dtype=np.uint8)
+        tier = ctypes.c_int32()
+        self._check(lib.tc_handle_read(self._h, h, i, buf.ctypes.data, ctypes.byref(tier)))
+        return buf.reshape(self.L, 2, self.chunk_bytes)
+
+    def handle_tier(self, h: int, i: int = 0) -> int:
+        """0 = host tier, 1 = peer tier (NEXT-2) for block i of an offloaded handle."""
+        buf = np.empty(self.block_bytes, dtype=np.uint8)
+        tier = ctypes.c_int32()
+        self._check(lib.tc_handle_read(self._h, h, i, buf.ctypes.data, ctypes.byref(tier)))
+        return tier.value
 
     def stats(self) -> dict:
         s = Stats()

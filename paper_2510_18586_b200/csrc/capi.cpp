@@ -41,6 +41,8 @@ void tc_pool_desc_init(tc_pool_desc *d, int32_t layers, int32_t kv_heads, int32_
     d->shard_world = 1;
     d->xfer_d2h = TC_XFER_AUTO;
     d->xfer_h2d = TC_XFER_AUTO;
+    d->peer_device = -1;
+    d->peer_slots = 0;
 }
 
 tc_status tc_pool_create_ex(const tc_pool_desc *d, tc_pool **out) {
@@ -110,7 +112,7 @@ tc_status tc_set_xfer_mode(tc_pool *p, int32_t d2h, int32_t h2d) {
 
 tc_status tc_set_launch_config(tc_pool *p, int32_t path, int32_t ctas, int32_t threads, int32_t variant) {
     TC_GUARD(p) {
-        if (path < 0 || path > 2 || threads < 32 || threads > 256 || threads % 32 || variant < 0 || variant > 3)
+        if (path < 0 || path > 3 || threads < 32 || threads > 256 || threads % 32 || variant < 0 || variant > 3)
             return TC_E_INVAL;
         P.ctas[path] = ctas;
         P.nthreads[path] = threads;
@@ -274,7 +276,32 @@ tc_status tc_handle_host(tc_pool *p, tc_handle h, int64_t i, const void **host_p
         auto it = P.handles.find(h);
         if (it == P.handles.end() || it->second.state != tc::kOffloaded) return TC_E_HANDLE;
         if (i < 0 || i >= (int64_t)it->second.slots.size() || !host_ptr) return TC_E_INVAL;
+        if (P.is_peer(it->second.slots[i])) return TC_E_INVAL;   // a peer-tier slot has no host address
         *host_ptr = P.host_ptr(it->second.slots[i]);
+        return TC_OK;
+    }
+    TC_CATCH
+}
+
+tc_status tc_handle_read(tc_pool *p, tc_handle h, int64_t i, void *dst, int32_t *tier) {
+    TC_GUARD(p) {
+        if (P.meta_only) return TC_E_NODEV;
+        auto it = P.handles.find(h);
+        if (it == P.handles.end() || it->second.state != tc::kOffloaded) return TC_E_HANDLE;
+        if (i < 0 || i >= (int64_t)it->second.slots.size() || !dst) return TC_E_INVAL;
+        const tc_status st = P.query(h, /*wait=*/true);
+        if (st != TC_OK) return st;
+        const int64_t slot = it->second.slots[i];
+        const bool pe = P.is_peer(slot);
+        if (tier) *tier = pe ? 1 : 0;
+        if (!pe) {
+            std::memcpy(dst, P.host_ptr(slot), (size_t)P.B);
+            return TC_OK;
+        }
+        if (cudaMemcpy(dst, P.peer_ptr(slot), (size_t)P.B, cudaMemcpyDeviceToHost) != cudaSuccess) {
+            cudaGetLastError();
+            return TC_E_CUDA;
+        }
         return TC_OK;
     }
     TC_CATCH
@@ -312,6 +339,12 @@ tc_status tc_stats(tc_pool *p, tc_stats_t *s) {
         s->bytes_h2d = P.bytes_h2d;
         s->xfer_d2h = P.mode_d2h;
         s->xfer_h2d = P.mode_h2d;
+        s->peer_slots = P.peer.count;
+        s->peer_free = (int64_t)P.peer.free_list.size();
+        int64_t prel = 0, hrel = 0;
+        for (int64_t x : P.slots.released) (P.is_peer(x) ? prel : hrel) += 1;
+        s->peer_used = P.peer.count - s->peer_free - prel;
+        s->host_used = P.slots.count - s->host_free - hrel;
         return TC_OK;
     }
     TC_CATCH

@@ -125,6 +125,7 @@ Pool::~Pool() {
         if (kv_.second.host) cudaFreeHost(kv_.second.host);
     if (ring_host) cudaFreeHost(ring_host);
     if (kts_dev) cudaFree(kts_dev);
+    if (peer.dev) cudaFree(peer.dev);
 }
 
 tc_status Pool::create(const tc_pool_desc &d) {
@@ -160,15 +161,21 @@ tc_status Pool::create(const tc_pool_desc &d) {
     mode_d2h = d.xfer_d2h;
     mode_h2d = d.xfer_h2d;
     if (mode_d2h < 0 || mode_d2h > 3 || mode_h2d < 0 || mode_h2d > 3) return TC_E_INVAL;
-    const char *path_names[3] = {"D2H", "H2D", "DEV"};
-    for (int i = 0; i < 3; ++i) {
+    // NEXT-2 peer tier (reading C1): slot ids S .. S+P-1, own LIFO free list (pops ascending)
+    if (d.peer_slots < 0 || (d.peer_slots > 0 && unbuffered)) return TC_E_INVAL;
+    peer.count = d.peer_slots;
+    peer.device = d.peer_device;
+    peer.free_list.resize(peer.count);
+    for (int64_t i = 0; i < peer.count; ++i) peer.free_list[i] = S + peer.count - 1 - i;
+    const char *path_names[4] = {"D2H", "H2D", "DEV", "PEER"};
+    for (int i = 0; i < 4; ++i) {
         char nm[32];
         std::snprintf(nm, sizeof nm, "TC_CTAS_%s", path_names[i]);
         ctas[i] = env_int(nm, 0);
         std::snprintf(nm, sizeof nm, "TC_THREADS_%s", path_names[i]);
         nthreads[i] = env_int(nm, 256);
         std::snprintf(nm, sizeof nm, "TC_VARIANT_%s", path_names[i]);
-        variant[i] = env_int(nm, i == 2 ? 3 : 0);   // device side: TMA bulk 4-stage (tier probe)
+        variant[i] = env_int(nm, i >= 2 ? 3 : 0);   // device side and peer tier: TMA bulk
     }
     if (meta_only) return TC_OK;
 
@@ -211,10 +218,24 @@ tc_status Pool::create(const tc_pool_desc &d) {
         cudaGetLastError(); ring_host = nullptr; return TC_E_OOM;
     }
     TC_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&ring_dev), ring_host, 0), "ring dev ptr");
+    if (peer.count > 0) {                     // the peer slab lives in the neighbour's HBM, reached over NVLink
+        if (peer.device < 0) return TC_E_INVAL;
+        if (peer.device != device) {
+            int ok = 0;
+            TC_CUDA(cudaDeviceCanAccessPeer(&ok, device, peer.device), "peer query");
+            if (!ok) return TC_E_INVAL;
+            const cudaError_t e = cudaDeviceEnablePeerAccess(peer.device, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "enable peer access");
+            cudaGetLastError();
+            TC_CUDA(cudaSetDevice(peer.device), "cudaSetDevice(peer)");
+        }
+        const cudaError_t e = cudaMalloc(&peer.dev, (size_t)(peer.count * B));
+        cudaSetDevice(device);
+        if (e != cudaSuccess) { cudaGetLastError(); peer.dev = nullptr; return TC_E_OOM; }
+    }
     staging_bytes = d.staging_bytes > 0 ? d.staging_bytes : (1ll << 30);
     if (staging_bytes < B) staging_bytes = B;
-    // AUTO: the copy-engine staged path measured faster than the SM direct path in both directions on B200
-    // (profiles/r01_xfer_probe.json: alone 57.1 vs 52.6 GB/s D2H, 55.4 vs 51.3 H2D; concurrent 53.7+49.7 vs 45+40).
+    // AUTO: the copy-engine staged path measured fastest for full cycles on B200 (profiles/r01_staged_ab.md).
     if (mode_d2h == TC_XFER_AUTO) mode_d2h = auto_mode(0);
     if (mode_h2d == TC_XFER_AUTO) mode_h2d = auto_mode(1);
     for (int i = 0; i < 16; ++i) {
@@ -730,6 +751,11 @@ tc_status Pool::agent_free(int32_t a) {
 tc_status Pool::plan_offload(OffPlan &P, int32_t na, const int32_t *ags, const int64_t *off, const int32_t *ids) {
     if (na < 1 || !ags || !off || !ids || off[0] != 0) return TC_E_INVAL;
     if (++epoch == 0) { std::fill(stamp.begin(), stamp.end(), 0); epoch = 1; }
+    // per item, in order (B1: the first failing item's status): validity, then the tier — the whole offload to the
+    // peer tier if its free list holds it, else to the CPU block buffer, else refused (reading C1)
+    const int64_t hf = (int64_t)slots.free_list.size(), pf = (int64_t)peer.free_list.size();
+    int64_t ht = 0, pt = 0;
+    std::vector<uint8_t> to_peer(na, 0);
     for (int32_t k = 0; k < na; ++k) {
         const int32_t a = ags[k];
         if (a < 0 || a >= max_agents || !agents[a].exists) return TC_E_INVAL;
@@ -740,12 +766,28 @@ tc_status Pool::plan_offload(OffPlan &P, int32_t na, const int32_t *ags, const i
                 return TC_E_INVAL;
             stamp[b] = epoch;
         }
-        if (!unbuffered && (int64_t)slots.free_list.size() < off[k + 1]) return TC_E_NOHOST;   // refuse
+        if (unbuffered) continue;
+        const int64_t m = off[k + 1] - off[k];
+        if (pf - pt >= m) {
+            to_peer[k] = 1;
+            pt += m;
+        } else if (hf - ht >= m) {
+            ht += m;
+        } else {
+            return TC_E_NOHOST;
+        }
     }
     P.na = na; P.ags = ags; P.off = off; P.ids = ids;
     const int64_t n = off[na];
     P.desc.resize(n);
     P.slot_of.resize(n);
+    P.host_taken = P.peer_taken = 0;
+    if (!unbuffered) {                                  // LIFO pop order per tier (A16)
+        for (int32_t k = 0; k < na; ++k)
+            for (int64_t i = off[k]; i < off[k + 1]; ++i)
+                P.slot_of[i] = to_peer[k] ? peer.free_list[pf - 1 - P.peer_taken++]
+                                          : slots.free_list[hf - 1 - P.host_taken++];
+    }
     if (unbuffered) {
         // Fig. 11 ablation: no CPU block buffer — pinned host memory is allocated for this offload now and freed
         // when its upload retires (the bursty OS allocation pattern of P:470-479).
@@ -762,13 +804,52 @@ tc_status Pool::plan_offload(OffPlan &P, int32_t na, const int32_t *ags, const i
         extra[next_slot] = ExtraSlab{h, dh, n, n};
         for (int64_t i = 0; i < n; ++i) P.slot_of[i] = next_slot + i;
         next_slot += n;
-    } else {
-        const size_t top = slots.free_list.size();
-        for (int64_t i = 0; i < n; ++i) P.slot_of[i] = slots.free_list[top - 1 - i];   // LIFO pop order (A16)
     }
     for (int32_t k = 0; k < na; ++k)
         for (int64_t i = off[k]; i < off[k + 1]; ++i)
             P.desc[i] = XferDesc{ids[i], ags[k] * max_bpa + alloc.own_pos[ids[i]], 0};
+    split_tiers(P.desc, P.slot_of, P.ts);
+    return TC_OK;
+}
+
+// Host-tier blocks keep their slot ids (the transfer engine resolves them); peer-tier blocks get ext = the peer slot.
+void Pool::split_tiers(const std::vector<XferDesc> &desc, const std::vector<int64_t> &slot_of, TierSplit &ts) const {
+    ts.hdesc.clear();
+    ts.hslot.clear();
+    ts.pdesc.clear();
+    if (peer.count == 0) return;                    // no peer tier: the plan's own vectors are used as they are
+    for (size_t i = 0; i < desc.size(); ++i) {
+        if (is_peer(slot_of[i])) {
+            XferDesc d = desc[i];
+            d.ext = reinterpret_cast<uint64_t>(peer_ptr(slot_of[i]));
+            ts.pdesc.push_back(d);
+        } else {
+            ts.hdesc.push_back(desc[i]);
+            ts.hslot.push_back(slot_of[i]);
+        }
+    }
+}
+
+// The peer-tier part of a batch: one device-side kernel on the direction's aux stream, started after the main
+// stream's waits; *join_ev = its completion (the main stream joins it after enqueueing the host-tier part).
+tc_status Pool::peer_launch(bool gather, const std::vector<XferDesc> &pd, cudaStream_t s, int32_t *join_ev) {
+    *join_ev = -1;
+    if (pd.empty() || meta_only) return TC_OK;
+    cudaStream_t aux = gather ? s_off_k : s_up_k;
+    int32_t e0;
+    tc_status st = ev_rec(s, &e0);
+    if (st != TC_OK) return st;
+    TC_CUDA(cudaStreamWaitEvent(aux, events[e0], 0), "peer wait");
+    const int32_t kind = gather ? 5 : 6;
+    cudaEvent_t t0;
+    if ((st = span_begin(aux, &t0)) != TC_OK) return st;
+    if ((st = launch_descs(gather, kind, 3, pd.data(), (int64_t)pd.size(), aux)) != TC_OK) return st;
+    if ((st = span_end(aux, kind, t0, (int64_t)pd.size() * B, /*link=*/false)) != TC_OK) return st;
+    return ev_rec(aux, join_ev);
+}
+
+tc_status Pool::join(cudaStream_t s, int32_t ev) {
+    if (ev >= 0) TC_CUDA(cudaStreamWaitEvent(s, events[ev], 0), "peer join");
     return TC_OK;
 }
 
@@ -789,7 +870,10 @@ tc_status Pool::offload_waits(const OffPlan &P) {
 // commit (a3 logical effects + a4 pending free); ev = the offload's completion event
 void Pool::commit_offload(const OffPlan &P, int32_t ev, tc_handle *out) {
     const int64_t n = P.off[P.na];
-    if (!unbuffered) slots.free_list.resize(slots.free_list.size() - n);
+    if (!unbuffered) {
+        slots.free_list.resize(slots.free_list.size() - P.host_taken);
+        peer.free_list.resize(peer.free_list.size() - P.peer_taken);
+    }
     for (int32_t k = 0; k < P.na; ++k) {
         const int32_t a = P.ags[k];
         AgentRec &ag = agents[a];
@@ -868,6 +952,7 @@ tc_status Pool::plan_upload(UpPlan &P, int32_t nh, const tc_handle *hs, const in
             P.slot_of[i] = P.hr[k]->slots[q];
         }
     }
+    split_tiers(P.desc, P.slot_of, P.ts);
     return TC_OK;
 }
 
@@ -919,7 +1004,12 @@ tc_status Pool::offload_batch(int32_t na, const int32_t *ags, const int64_t *off
     int32_t ev = -1;
     if (!meta_only) {
         if ((st = offload_waits(P)) != TC_OK) return st;
-        if ((st = enqueue_xfer(true, mode_d2h, P.desc, P.slot_of, s_off)) != TC_OK) return st;
+        int32_t pj;
+        if ((st = peer_launch(true, P.ts.pdesc, s_off, &pj)) != TC_OK) return st;
+        if ((st = enqueue_xfer(true, mode_d2h, peer.count ? P.ts.hdesc : P.desc, peer.count ? P.ts.hslot : P.slot_of,
+                               s_off)) != TC_OK)
+            return st;
+        if ((st = join(s_off, pj)) != TC_OK) return st;
         if ((st = ev_rec(s_off, &ev)) != TC_OK) return st;
     }
     commit_offload(P, ev, out);
@@ -935,7 +1025,12 @@ tc_status Pool::upload_batch(int32_t nh, const tc_handle *hs, const int64_t *off
     int32_t ev = -1;
     if (!meta_only) {
         if ((st = upload_waits(P)) != TC_OK) return st;
-        if ((st = enqueue_xfer(false, mode_h2d, P.desc, P.slot_of, s_up)) != TC_OK) return st;
+        int32_t pj;
+        if ((st = peer_launch(false, P.ts.pdesc, s_up, &pj)) != TC_OK) return st;
+        if ((st = enqueue_xfer(false, mode_h2d, peer.count ? P.ts.hdesc : P.desc, peer.count ? P.ts.hslot : P.slot_of,
+                               s_up)) != TC_OK)
+            return st;
+        if ((st = join(s_up, pj)) != TC_OK) return st;
         if ((st = ev_rec(s_up, &ev)) != TC_OK) return st;
     }
     commit_upload(P, ev, out_ids);
@@ -963,20 +1058,30 @@ tc_status Pool::cycle(int32_t nh, const tc_handle *hs, const int64_t *up_off, in
     int32_t ev_up = -1, ev_off = -1;
     if (!meta_only) {
         XferJob ju, jo;
+        int32_t pu = -1, po = -1;                                     // peer-tier parts (NEXT-2)
+        const bool pt = peer.count > 0;
         if (nh > 0) {
             if ((st = upload_waits(U)) != TC_OK) return st;
-            if ((st = xfer_init(ju, false, mode_h2d, &U.desc, &U.slot_of, s_up)) != TC_OK) return st;
+            if ((st = peer_launch(false, U.ts.pdesc, s_up, &pu)) != TC_OK) return st;
+            if ((st = xfer_init(ju, false, mode_h2d, pt ? &U.ts.hdesc : &U.desc, pt ? &U.ts.hslot : &U.slot_of,
+                                s_up)) != TC_OK)
+                return st;
             if ((st = xfer_phase_a(ju)) != TC_OK) return st;          // H2D copies start first
         }
         if (na > 0) {
             if ((st = offload_waits(O)) != TC_OK) return st;
-            if ((st = xfer_init(jo, true, mode_d2h, &O.desc, &O.slot_of, s_off)) != TC_OK) return st;
+            if ((st = peer_launch(true, O.ts.pdesc, s_off, &po)) != TC_OK) return st;
+            if ((st = xfer_init(jo, true, mode_d2h, pt ? &O.ts.hdesc : &O.desc, pt ? &O.ts.hslot : &O.slot_of,
+                                s_off)) != TC_OK)
+                return st;
             if ((st = xfer_phase_a(jo)) != TC_OK) return st;          // gathers
             if ((st = xfer_phase_b(jo)) != TC_OK) return st;          // D2H copies
+            if ((st = join(s_off, po)) != TC_OK) return st;
             if ((st = ev_rec(s_off, &ev_off)) != TC_OK) return st;
         }
         if (nh > 0) {
             if ((st = xfer_phase_b(ju)) != TC_OK) return st;          // scatters + remap
+            if ((st = join(s_up, pu)) != TC_OK) return st;
             if ((st = ev_rec(s_up, &ev_up)) != TC_OK) return st;
         }
     }
@@ -1096,6 +1201,10 @@ tc_status Pool::sync() {
     for (auto it = slots.released.rbegin(); it != slots.released.rend(); ++it) {
         if (*it < slots.count) {
             slots.free_list.push_back(*it);
+            continue;
+        }
+        if (is_peer(*it)) {                                // peer-tier slot: back to its own free list
+            peer.free_list.push_back(*it);
             continue;
         }
         auto sl = std::prev(extra.upper_bound(*it));      // unbuffered ablation: free the slab with its last block

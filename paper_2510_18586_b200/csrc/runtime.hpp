@@ -49,6 +49,14 @@ struct HostSlots {
     std::vector<int64_t> released;   // returned to free_list at tc_sync
 };
 
+// NEXT-2 peer tier: block-shard slots in a neighbouring GPU's HBM, ids S .. S+count-1, own LIFO free list.
+struct PeerSlots {
+    char *dev = nullptr;             // base of the slab on `device` (peer-accessible from the pool's device)
+    int device = -1;
+    int64_t count = 0;
+    std::vector<int64_t> free_list;  // back() = next slot handed out
+};
+
 struct AgentRec {
     bool exists = false;
     int32_t cls = 0;
@@ -102,12 +110,15 @@ struct Pool {
 
     // transfer modes
     int32_t mode_d2h = TC_XFER_DIRECT, mode_h2d = TC_XFER_DIRECT;
-    // launch config per path: [0] direct D2H, [1] direct H2D, [2] device tier + staged kernels
-    int ctas[3] = {0, 0, 0}, nthreads[3] = {256, 256, 256}, variant[3] = {0, 0, 0};
+    // launch config per path: [0] direct D2H, [1] direct H2D, [2] device tier + staged kernels, [3] peer tier
+    int ctas[4] = {0, 0, 0, 0}, nthreads[4] = {256, 256, 256, 256}, variant[4] = {0, 0, 3, 3};
 
     // bookkeeping
     BlockAllocator alloc;
     HostSlots slots;
+    PeerSlots peer;
+    bool is_peer(int64_t slot) const { return peer.count > 0 && slot >= slots.count; }
+    char *peer_ptr(int64_t slot) const { return peer.dev + (slot - slots.count) * B; }
     std::vector<AgentRec> agents;
     int32_t n_agents = 0;
     std::unordered_map<uint64_t, HandleRec> handles;
@@ -159,12 +170,20 @@ struct Pool {
     tc_status upload_batch(int32_t nh, const tc_handle *hs, const int64_t *offsets, int32_t *out_ids);
     tc_status cycle(int32_t nh, const tc_handle *hs, const int64_t *up_off, int32_t *out_ids, int32_t na,
                     const int32_t *ags, const int64_t *off_off, const int32_t *ids, tc_handle *out_h);
+    // A batch's blocks split by tier: host-tier descriptors + slots (copy engine / direct kernel) and peer-tier
+    // descriptors (ext = the peer slot's device address; one device-side kernel).
+    struct TierSplit {
+        std::vector<XferDesc> hdesc, pdesc;
+        std::vector<int64_t> hslot;
+    };
     struct OffPlan {
         int32_t na = 0;
         const int32_t *ags = nullptr, *ids = nullptr;
         const int64_t *off = nullptr;
         std::vector<XferDesc> desc;
         std::vector<int64_t> slot_of;
+        int64_t host_taken = 0, peer_taken = 0;
+        TierSplit ts;
     };
     struct UpPlan {
         int32_t nh = 0;
@@ -176,7 +195,11 @@ struct Pool {
         std::vector<int32_t> dst;
         std::vector<XferDesc> desc;
         std::vector<int64_t> slot_of;
+        TierSplit ts;
     };
+    void split_tiers(const std::vector<XferDesc> &desc, const std::vector<int64_t> &slot_of, TierSplit &ts) const;
+    tc_status peer_launch(bool gather, const std::vector<XferDesc> &pd, cudaStream_t s, int32_t *join_ev);
+    tc_status join(cudaStream_t s, int32_t ev);
     tc_status plan_offload(OffPlan &P, int32_t na, const int32_t *ags, const int64_t *off, const int32_t *ids);
     tc_status offload_waits(const OffPlan &P);
     void commit_offload(const OffPlan &P, int32_t ev, tc_handle *out);

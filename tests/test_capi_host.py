@@ -39,19 +39,20 @@ def test_strerror_and_status_codes():
     assert tcb.lib.tc_strerror(0).decode() == "ok"
 
 
-def meta_pool(N, S, ncls=N_CLASSES, max_bpa=4096, L=1, H=2, D=64):
+def meta_pool(N, S, ncls=N_CLASSES, max_bpa=4096, L=1, H=2, D=64, P=0):
     return tcb.Pool(L, H, D, 16, "fp16", N, device=-1, host_slots=S, n_classes=ncls, max_agents=1024,
-                    max_blocks_per_agent=max_bpa)
+                    max_blocks_per_agent=max_bpa, peer_slots=P)
 
 
 def stats_view(s):
-    return {k: s[k] for k in ("free", "alloc", "pending", "reserved_blocks", "host_free", "host_used", "reserved",
-                              "claimed")}
+    return {k: s[k] for k in ("free", "alloc", "pending", "reserved_blocks", "host_free", "host_used", "peer_free",
+                              "peer_used", "reserved", "claimed")}
 
 
-def replay_both(ops, N, S, ncls=N_CLASSES, max_bpa=4096):
-    o = OraclePool(N, S, n_classes=ncls, max_agents=1024, max_blocks_per_agent=max_bpa, store=ProvStore(N, S))
-    c = meta_pool(N, S, ncls, max_bpa)
+def replay_both(ops, N, S, ncls=N_CLASSES, max_bpa=4096, P=0):
+    o = OraclePool(N, S, n_classes=ncls, max_agents=1024, max_blocks_per_agent=max_bpa, store=ProvStore(N, S + P),
+                   n_peer_slots=P)
+    c = meta_pool(N, S, ncls, max_bpa, P=P)
     ro, rc = Replayer(o), Replayer(c)
     for i, op in enumerate(ops):
         a, b = ro.step(op), rc.step(op)
@@ -79,6 +80,50 @@ def test_fuzz_scripts_match_oracle(seed):
     ops = fuzz_script(seed, n_ops=150, n_agents=3, n_classes=2, N=N, max_alloc=int(rng.choice([2, 6, 12])),
                       gradual=seed % 2 == 1)
     replay_both(ops, N, S, ncls=2, max_bpa=int(rng.choice([8, 4096])))
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_fuzz_scripts_with_peer_tier_match_oracle(seed):
+    """NEXT-2 peer tier (reading C1): tier placement, per-tier slot counts and refusals identical to the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    N = int(rng.choice([16, 40]))
+    S, P = int(rng.choice([3, 8])), int(rng.choice([2, 5, 12]))
+    ops = fuzz_script(500 + seed, n_ops=150, n_agents=3, n_classes=2, N=N, max_alloc=int(rng.choice([2, 6])),
+                      gradual=seed % 3 == 0)
+    replay_both(ops, N, S, ncls=2, P=P)
+
+
+def test_peer_tier_worked_example_through_capi():
+    """tests/golden/next2_peer_tier.json through the C ABI (metadata-only pool): placement and counters."""
+    import json
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "next2_peer_tier.json")))
+    c = meta_pool(g["N"], g["S"], P=g["P"])
+    c.agent_add(0, 0)
+    c.agent_add(1, 1)
+    for st in g["steps"]:
+        if st["op"] == "alloc":
+            assert list(c.alloc(st["agent"], st["n"])) == st["expect"]
+        elif st["op"] == "offload":
+            if "expect_status" in st:
+                with pytest.raises(tcb.TcError) as e:
+                    c.offload(st["agent"], st["ids"])
+                assert e.value.status == tcb.E_NOHOST
+                continue
+            c.offload(st["agent"], st["ids"])
+        elif st["op"] == "upload":
+            assert list(c.upload(st["handle"])) == st["expect"]
+        elif st["op"] == "sync":
+            c.sync()
+        s = c.stats()
+        if "expect_peer_free" in st:
+            assert (s["peer_free"], s["host_free"]) == (st["expect_peer_free"], st["expect_host_free"]), st
+    assert (c.stats()["peer_used"], c.stats()["host_used"]) == (4, 6)
+
+
+def test_peer_tier_rejected_with_unbuffered_ablation():
+    with pytest.raises(tcb.TcError) as e:
+        tcb.Pool(1, 2, 64, 16, "fp16", 8, device=-1, host_slots=4, peer_slots=2, unbuffered=True)
+    assert e.value.status == tcb.E_INVAL
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])

@@ -37,10 +37,11 @@ def _cuda():
 
 
 def dev_pool(L, H, D, N, S, mode="direct", ncls=N_CLASSES, max_bpa=4096, seed=1, rank=0, world=1, staging=0,
-             dtype="bf16", T=16):
+             dtype="bf16", T=16, P=0):
     d2h, h2d, variant = MODES[mode]
     p = tcb.Pool(L, H, D, T, dtype, N, device=0, shard_rank=rank, shard_world=world, host_slots=S, n_classes=ncls,
-                 max_agents=1024, max_blocks_per_agent=max_bpa, xfer_d2h=d2h, xfer_h2d=h2d, staging_bytes=staging)
+                 max_agents=1024, max_blocks_per_agent=max_bpa, xfer_d2h=d2h, xfer_h2d=h2d, staging_bytes=staging,
+                 peer_device=0 if P else -1, peer_slots=P)
     for path in range(3):
         p.set_launch_config(path, 0, 256, variant)
     p.fill(seed)
@@ -56,7 +57,8 @@ def compare_full(o: OraclePool, c: tcb.Pool, where=""):
     for a, ag in o.agents.items():
         assert tab[a, :len(ag.table)].tolist() == ag.table, (where, a)
     so, sc = o.stats(), c.stats()
-    for k in ("free", "alloc", "pending", "reserved_blocks", "host_free", "host_used", "reserved", "claimed"):
+    for k in ("free", "alloc", "pending", "reserved_blocks", "host_free", "host_used", "peer_free", "peer_used",
+              "reserved", "claimed"):
         assert so[k] == sc[k], (where, k)
 
 
@@ -69,10 +71,11 @@ def compare_live_host(o: OraclePool, c: tcb.Pool, where=""):
             assert np.array_equal(c.handle_host_bytes(h, i), o.store.host[s]), (where, h, i)
 
 
-def run_script(ops, L, H, D, N, S, mode, ncls=N_CLASSES, max_bpa=4096, seed=1, staging=0, T=16):
+def run_script(ops, L, H, D, N, S, mode, ncls=N_CLASSES, max_bpa=4096, seed=1, staging=0, T=16, P=0):
     pool0 = content.pool_bytes(seed, L, N, T, H, D)
-    o = OraclePool(N, S, n_classes=ncls, max_agents=1024, max_blocks_per_agent=max_bpa, store=BytesStore(pool0, S))
-    c = dev_pool(L, H, D, N, S, mode, ncls, max_bpa, seed, staging=staging, T=T)
+    o = OraclePool(N, S, n_classes=ncls, max_agents=1024, max_blocks_per_agent=max_bpa,
+                   store=BytesStore(pool0, S + P), n_peer_slots=P)
+    c = dev_pool(L, H, D, N, S, mode, ncls, max_bpa, seed, staging=staging, T=T, P=P)
     assert np.array_equal(c.kv_tensor().cpu().numpy(), pool0), "fill kernel != content generator"
     ro, rc = Replayer(o), Replayer(c)
     for i, op in enumerate(ops):
@@ -264,3 +267,26 @@ def test_batches_above_one_launch_capacity(monkeypatch, mode):
     torch.cuda.synchronize()
     exp = np.take(o.store.pool, ids, axis=2).transpose(2, 0, 1, 3)
     assert np.array_equal(dst.cpu().numpy().reshape(exp.shape), exp)
+
+
+@pytest.mark.parametrize("mode", ["staged", "direct", "copy", "staged_tile"])
+@pytest.mark.parametrize("gi", [0, 2, 4])
+def test_peer_tier_fuzz_bytes(mode, gi):
+    """NEXT-2 peer tier (reading C1) with the peer slab on this same GPU (the single-GPU stand-in for a neighbour's
+    HBM): tier placement, peer-slot images, pool bytes, tables and counters against the oracle after every sync; the
+    host-tier part of each batch still takes `mode`'s path."""
+    L, H, D, N, S, T = GEOMS[gi]
+    for seed in range(2):
+        ops = fuzz_script(seed + 31 * gi, n_ops=90, n_agents=3, n_classes=N_CLASSES, N=N, max_alloc=6)
+        o, c = run_script(ops, L, H, D, N, S, mode, seed=seed + 5, T=T, P=max(2, S // 2))
+        assert c.stats()["peer_slots"] == max(2, S // 2)
+
+
+def test_peer_tier_cycles_mixed_tiers():
+    """tc_cycle batches whose offloads split across both tiers (peer slots fill up mid-batch), over C2-shaped
+    blocks: bytes and tables against the oracle."""
+    cfg = CONFIGS["c2"].scaled(N=512, host_slots=160, bg_fill=0.3)
+    ops = build_script(cfg, 10, combined=True)
+    L, H, D = cfg.L, cfg.H, cfg.D
+    o, c = run_script(ops, L, H, D, cfg.N, cfg.host_slots(), "staged", seed=2, P=96)
+    assert any(x >= cfg.host_slots() for h in o.handles.values() for x in h.slots)
