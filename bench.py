@@ -312,13 +312,13 @@ def run_ours(args):
     e2e = all_bytes / (host_total_ms * 1e-3) / 1e9
     # roofline of the dominant kernel: per-launch algorithmic bytes / the launch's device duration
     stats = pool.stats()
-    link_bound = {"offload_kernel": stats["xfer_d2h"] == tcb.XFER_DIRECT,
-                  "upload_kernel": stats["xfer_h2d"] == tcb.XFER_DIRECT,
-                  "offload_peer_kernel": False, "upload_peer_kernel": False}
+    link_bound = {"offload_kernel": False, "upload_kernel": False, "offload_peer_kernel": False,
+                  "upload_peer_kernel": False, "offload_direct_kernel": True, "upload_direct_kernel": True}
     kern = {}
     self_peer = args.peer and peer_dev == local
-    for k, peak_key in (("offload_kernel", "d2h_gbs"), ("upload_kernel", "h2d_gbs"),
-                        ("offload_peer_kernel", None), ("upload_peer_kernel", None)):
+    for k, peak_key in (("offload_kernel", None), ("upload_kernel", None), ("offload_peer_kernel", None),
+                        ("upload_peer_kernel", None), ("offload_direct_kernel", "d2h_gbs"),
+                        ("upload_direct_kernel", "h2d_gbs")):
         # kernel duration = first CTA start -> last CTA end on the device clock (%globaltimer), recorded by the
         # kernel itself on the stream it runs on; the CUDA-event span around the launch (which also counts host
         # launch latency when the stream was idle) is kept beside it

@@ -56,7 +56,8 @@ typedef enum {
 } tc_status;
 
 typedef enum {
-    TC_XFER_AUTO = 0,    /* per direction: the path measured fastest for the cycle on B200 */
+    TC_XFER_AUTO = 0,    /* per direction: STAGED, the path measured fastest for the cycle on B200, except that a
+                            batch of <= 2 MiB takes DIRECT (one launch, lower latency) */
     TC_XFER_DIRECT = 1,  /* one SM kernel reads/writes mapped pinned host memory over the host link */
     TC_XFER_STAGED = 2,  /* SM gather/scatter to a device staging ring + copy-engine cudaMemcpyAsync */
     TC_XFER_COPY = 3     /* the copy engine moves each block as one strided DMA (2L rows of C bytes, row pitch N*C in
@@ -208,11 +209,11 @@ tc_status tc_handle_host(tc_pool *p, tc_handle h, int64_t i, const void **host_p
 tc_status tc_handle_read(tc_pool *p, tc_handle h, int64_t i, void *dst, int32_t *tier);
 tc_status tc_stats(tc_pool *p, tc_stats_t *s);
 /* Per-launch device timing (CUDA events recorded on the launching stream around every kernel / memcpy run).
-   Spans complete at tc_sync, where their durations are accumulated.  Index (TC_NKINDS): 0 offload kernels (direct
-   mode: the whole transfer; staged mode: the device-side gather), 1 upload kernels (likewise; scatter), 2
-   device-tier kernels, 3 D2H memcpy (staged / copy mode), 4 H2D memcpy, 5 peer-tier offload kernels, 6 peer-tier
-   upload kernels.  bytes = KV payload bytes moved (n * B). */
-#define TC_NKINDS 7
+   Spans complete at tc_sync, where their durations are accumulated.  Index (TC_NKINDS): 0 staged-mode device-side
+   gather kernels (offload), 1 staged-mode scatter kernels (upload), 2 device-tier kernels, 3 D2H memcpy (staged /
+   copy mode), 4 H2D memcpy, 5 peer-tier offload kernels, 6 peer-tier upload kernels, 7 direct-mode offload kernels
+   (mapped host memory: the whole transfer), 8 direct-mode upload kernels.  bytes = KV payload bytes moved (n * B). */
+#define TC_NKINDS 9
 typedef struct tc_timing_t {
     double ms[TC_NKINDS];
     int64_t count[TC_NKINDS];

@@ -59,9 +59,9 @@ class PoolDesc(ctypes.Structure):
 
 
 class Timing(ctypes.Structure):
-    _fields_ = [("ms", ctypes.c_double * 7), ("count", ctypes.c_int64 * 7), ("bytes", ctypes.c_int64 * 7),
-                ("kernel_ms", ctypes.c_double * 7), ("kernel_count", ctypes.c_int64 * 7),
-                ("kernel_bytes", ctypes.c_int64 * 7)]
+    _fields_ = [("ms", ctypes.c_double * 9), ("count", ctypes.c_int64 * 9), ("bytes", ctypes.c_int64 * 9),
+                ("kernel_ms", ctypes.c_double * 9), ("kernel_count", ctypes.c_int64 * 9),
+                ("kernel_bytes", ctypes.c_int64 * 9)]
 
 
 class Span(ctypes.Structure):
@@ -70,8 +70,8 @@ class Span(ctypes.Structure):
 
 
 TIMING_KINDS = ("offload_kernel", "upload_kernel", "device_kernel", "memcpy_d2h", "memcpy_h2d", "offload_peer_kernel",
-                "upload_peer_kernel")
-KERNEL_KINDS = (0, 1, 2, 5, 6)
+                "upload_peer_kernel", "offload_direct_kernel", "upload_direct_kernel")
+KERNEL_KINDS = (0, 1, 2, 5, 6, 7, 8)
 
 
 class Stats(ctypes.Structure):

@@ -103,8 +103,10 @@ tc_status tc_streams(tc_pool *p, void **upload_stream, void **offload_stream) {
 tc_status tc_set_xfer_mode(tc_pool *p, int32_t d2h, int32_t h2d) {
     TC_GUARD(p) {
         if (d2h < 0 || d2h > 3 || h2d < 0 || h2d > 3) return TC_E_INVAL;
-        P.mode_d2h = d2h == TC_XFER_AUTO ? P.auto_mode(0) : d2h;
-        P.mode_h2d = h2d == TC_XFER_AUTO ? P.auto_mode(1) : h2d;
+        P.auto_dir[0] = d2h == TC_XFER_AUTO;
+        P.auto_dir[1] = h2d == TC_XFER_AUTO;
+        P.mode_d2h = P.auto_dir[0] ? P.auto_mode(0) : d2h;
+        P.mode_h2d = P.auto_dir[1] ? P.auto_mode(1) : h2d;
         return TC_OK;
     }
     TC_CATCH

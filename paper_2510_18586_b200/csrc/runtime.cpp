@@ -236,8 +236,11 @@ tc_status Pool::create(const tc_pool_desc &d) {
     staging_bytes = d.staging_bytes > 0 ? d.staging_bytes : (1ll << 30);
     if (staging_bytes < B) staging_bytes = B;
     // AUTO: the copy-engine staged path measured fastest for full cycles on B200 (profiles/r01_staged_ab.md).
-    if (mode_d2h == TC_XFER_AUTO) mode_d2h = auto_mode(0);
-    if (mode_h2d == TC_XFER_AUTO) mode_h2d = auto_mode(1);
+    auto_dir[0] = mode_d2h == TC_XFER_AUTO;
+    auto_dir[1] = mode_h2d == TC_XFER_AUTO;
+    if (auto_dir[0]) mode_d2h = auto_mode(0);
+    if (auto_dir[1]) mode_h2d = auto_mode(1);
+    auto_direct_bytes = env_int("TC_AUTO_DIRECT_KIB", 2048) * 1024ll;
     for (int i = 0; i < 16; ++i) {
         cudaEvent_t e;
         TC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -299,7 +302,7 @@ void Pool::spans_collect() {
             tacc.count[sp.kind] += 1;
             tacc.bytes[sp.kind] += sp.bytes;
             if (sp.link && B > 0) {                             // the host-link side of a transfer
-                const int dir = (sp.kind == 0 || sp.kind == 3) ? 0 : 1;
+                const int dir = (sp.kind == 7 || sp.kind == 3) ? 0 : 1;
                 cal_ms[dir] += ms;
                 cal_blocks[dir] += sp.bytes / B;
             }
@@ -410,6 +413,7 @@ tc_status Pool::xfer_init(XferJob &j, bool gather, int32_t mode, const std::vect
     j.slot_of = slot_of;
     j.s = s;
     j.n = (int64_t)desc->size();
+    if (j.mode == TC_XFER_STAGED && auto_dir[gather ? 0 : 1] && j.n * B <= auto_direct_bytes) j.mode = TC_XFER_DIRECT;
     if (j.mode != TC_XFER_STAGED || j.n == 0) return TC_OK;
     const int dir = gather ? 0 : 1;
     if (!staging[dir]) TC_CUDA(cudaMalloc(&staging[dir], staging_bytes), "staging alloc");
@@ -448,6 +452,8 @@ tc_status Pool::xfer_init(XferJob &j, bool gather, int32_t mode, const std::vect
 }
 
 // AUTO: the path measured fastest for a full scheduling cycle on B200 (both directions concurrently).
+// A batch of at most auto_direct_bytes still takes the DIRECT kernel: one launch instead of kernel + DMA, ~5 µs
+// sooner for 1-2 blocks and equal from ~2 MiB up (profiles/r01_sweep_c{2,5}.json).
 int32_t Pool::auto_mode(int dir) const {
     return env_int(dir == 0 ? "TC_AUTO_D2H" : "TC_AUTO_H2D", TC_XFER_STAGED);
 }
@@ -598,7 +604,7 @@ tc_status Pool::xfer_phase_a(XferJob &j) {
     if (j.mode == TC_XFER_DIRECT) {
         const bool dev_tier = j.slot_of == nullptr || j.slot_of->empty();
         const int path = dev_tier ? 2 : (j.gather ? 0 : 1);
-        const int32_t kind = dev_tier ? 2 : (j.gather ? 0 : 1);
+        const int32_t kind = dev_tier ? 2 : (j.gather ? 7 : 8);
         const XferDesc *d = j.desc->data();
         if (!dev_tier) {
             cd_.resize((size_t)j.n);

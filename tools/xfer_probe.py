@@ -51,7 +51,8 @@ def main():
             if rep:
                 out.append((tim, t1 - t0))
         agg = {}
-        for k in ("offload_kernel", "upload_kernel", "memcpy_d2h", "memcpy_h2d"):
+        for k in ("offload_kernel", "upload_kernel", "offload_direct_kernel", "upload_direct_kernel", "memcpy_d2h",
+                  "memcpy_h2d"):
             ms = [t[k][0] for t, _ in out if t[k][1]]
             by = [t[k][2] for t, _ in out if t[k][1]]
             if ms:
