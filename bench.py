@@ -116,6 +116,24 @@ class Clocks:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
+def bind_numa_local(index: int) -> str:
+    """Pin this rank's threads to the CPUs NVML reports as local to GPU `index`, before any pinned allocation, so the
+    CPU block buffer (cudaHostAlloc, first touch) lands in the GPU's own NUMA node and each GPU's host traffic stays
+    on its own socket's memory (matters at 8 GPUs; a no-op on a 1-socket box)."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        cpus &= set(range(os.cpu_count()))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+        return f"{len(cpus)} cpus local to GPU {index}"
+    except Exception as e:  # noqa: BLE001 - affinity is an optimisation, never a failure
+        return f"unbound ({type(e).__name__})"
+
+
 def hostlink_peak(torch, dev, nbytes=1 << 30, reps=5):
     """Pinned cudaMemcpyAsync D2H / H2D / bidirectional, best of `reps`."""
     h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
@@ -163,6 +181,7 @@ def run_ours(args):
     import paper_2510_18586_b200 as tcb
 
     rank, world, local = dist_env()
+    numa = bind_numa_local(local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
@@ -388,6 +407,7 @@ def run_ours(args):
                    "xfer": XFER_NAMES[stats["xfer_d2h"]] + "/" + XFER_NAMES[stats["xfer_h2d"]],
                    "l2": "flushed between steps (256 MiB write, outside the step events)",
                    "parallelism": f"{world} independent ranks" + (f", head-sharded G={G}" if G > 1 else ""),
+                   "numa": numa,
                    "offload_tier": ("peer slots on GPU %d (%s) first, then host" % (
                        peer_dev, "this GPU's own HBM" if peer_dev == local else "NVLink neighbour")) if args.peer
                    else "host"},

@@ -212,7 +212,10 @@ class Pool:
         if getattr(self, "_h", None):
             lib.tc_pool_destroy(self._h)
             self._h = None
-        self._keep = []
+        if self._keep:
+            self._keep = []
+            import torch   # hand the pool's HBM back (the caching allocator would keep tens of GiB reserved)
+            torch.cuda.empty_cache()
 
     def __del__(self):
         try:

@@ -183,7 +183,7 @@ def sample_check(c: tcb.Pool, cfg, prov: np.ndarray, blocks: np.ndarray, seed: i
         assert np.array_equal(got[k], exp), (cfg.name, int(bl[k]), int(lk[k]))
 
 
-@pytest.mark.parametrize("name,world", [("c2", 1), ("c3", 1), ("c4", 8), ("c5", 8)])
+@pytest.mark.parametrize("name,world", [("c2", 1), ("c3", 1), ("c4", 1), ("c4", 8), ("c5", 8)])
 def test_full_size_config_parity(name, world):
     cfg = CONFIGS[name]
     rank = world - 1 if world > 1 else 0
