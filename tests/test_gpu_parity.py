@@ -290,3 +290,48 @@ def test_peer_tier_cycles_mixed_tiers():
     L, H, D = cfg.L, cfg.H, cfg.D
     o, c = run_script(ops, L, H, D, cfg.N, cfg.host_slots(), "staged", seed=2, P=96)
     assert any(x >= cfg.host_slots() for h in o.handles.values() for x in h.slots)
+
+
+def test_c1_many_seeds_auto():
+    """C1 geometry, 1000 seeded fuzz scripts through the default AUTO path (staged, with the
+    small-batch direct kernel), a tiny staging buffer so ring reuse engages: pool bytes, tables and counters equal
+    the oracle's at the end of every script."""
+    L, H, D, T, N, S = 1, 2, 64, 16, 64, 16
+    for seed in range(1000):
+        ops = fuzz_script(seed + 5000, n_ops=40, n_agents=2, n_classes=2, N=N, max_alloc=8, gradual=seed % 4 == 0)
+        pool0 = content.pool_bytes(seed, L, N, T, H, D)
+        o = OraclePool(N, S, n_classes=2, max_agents=1024, max_blocks_per_agent=4096, store=BytesStore(pool0, S))
+        c = tcb.Pool(L, H, D, T, "fp16", N, device=0, host_slots=S, n_classes=2, staging_bytes=4 * 8192)
+        c.fill(seed)
+        ro, rc = Replayer(o), Replayer(c)
+        for i, op in enumerate(ops):
+            a, b = ro.step(op), rc.step(op)
+            assert a == b, (seed, i, op, a, b)
+        c.sync()
+        o.sync()
+        compare_full(o, c, f"seed {seed}")
+        c.close()
+
+
+def test_head_shards_concatenate_to_unsharded_run():
+    """SURVEY.md §4 item 6 (sharding without 8 GPUs): G = 4 head-shard pools and one unsharded pool on this GPU run
+    the same script; the shards' pools, concatenated along the head axis, equal the unsharded pool byte for byte,
+    and all tables agree (the multi-GPU layout is correct by construction)."""
+    L, H, D, T, N, S, G = 3, 8, 64, 16, 48, 24, 4
+    ops = fuzz_script(77, n_ops=120, n_agents=3, n_classes=2, N=N, max_alloc=6)
+    pools = []
+    for r, w in [(0, 1)] + [(r, G) for r in range(G)]:
+        c = tcb.Pool(L, H, D, T, "bf16", N, device=0, shard_rank=r, shard_world=w, host_slots=S, n_classes=2)
+        c.fill(13)
+        tr = Replayer(c).run(ops)
+        c.sync()
+        pools.append((c, tr))
+    full = pools[0][0].kv_tensor().cpu().numpy().reshape(L, 2, N, T, H, D * 2)
+    shards = [p.kv_tensor().cpu().numpy().reshape(L, 2, N, T, H // G, D * 2) for p, _ in pools[1:]]
+    assert np.array_equal(np.concatenate(shards, axis=4), full)
+    for p, tr in pools[1:]:
+        assert tr == pools[0][1]
+        for a in range(3):
+            assert p.block_table(a) == pools[0][0].block_table(a)
+    for p, _ in pools:
+        p.close()
