@@ -59,7 +59,7 @@ typedef enum {
     TC_XFER_AUTO = 0,    /* per direction: STAGED, the path measured fastest for the cycle on B200, except that a
                             batch of <= 2 MiB takes DIRECT (one launch, lower latency) */
     TC_XFER_DIRECT = 1,  /* one SM kernel reads/writes mapped pinned host memory over the host link */
-    TC_XFER_STAGED = 2,  /* SM gather/scatter to a device staging ring + copy-engine cudaMemcpyAsync */
+    TC_XFER_STAGED = 2,  /* TMA gather/scatter to a device staging buffer + batched copy-engine DMA */
     TC_XFER_COPY = 3     /* the copy engine moves each block as one strided DMA (2L rows of C bytes, row pitch N*C in
                             the pool) straight between the pool and its pinned slot; a small kernel rewrites the
                             block table (offload: before the DMA; upload: after it) */
@@ -80,8 +80,9 @@ typedef struct tc_pool_desc {
                                     16-byte aligned; NULL -> library cudaMalloc */
     int32_t *table_dev;          /* optional external device int32[max_agents][max_blocks_per_agent]; NULL -> own */
     int32_t xfer_d2h, xfer_h2d;  /* tc_xfer_mode per direction */
-    int64_t staging_bytes;       /* device staging ring per direction for STAGED mode; 0 -> 256 MiB */
-    int64_t desc_bytes;          /* pinned descriptor ring; 0 -> 16 MiB */
+    int64_t staging_bytes;       /* device staging buffer per direction for STAGED mode (allocated on first use); a
+                                    larger batch runs double-buffered halves; 0 -> 1 GiB */
+    int64_t desc_bytes;          /* pinned ring for block-table pushes (tc_alloc growth); 0 -> 16 MiB */
     int32_t unbuffered;          /* ABLATION ONLY (Fig. 11): no CPU block buffer — each offload
                                     cudaHostAlloc's its own pinned memory, freed (cudaFreeHost) when its upload
                                     retires; the bursty host allocation pattern of P:470-479.  0 = normal. */

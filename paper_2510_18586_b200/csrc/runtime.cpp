@@ -1254,7 +1254,7 @@ tc_status Pool::device_tier(bool gather, const int32_t *ids, int64_t n, void *ex
     }
     if (s && s != s_off && s != s_up && s != s_compute &&
         std::find(foreign.begin(), foreign.end(), s) == foreign.end())
-        foreign.push_back(s);   // ring wrap must also wait for descriptor reads on caller streams
+        foreign.push_back(s);   // tc_sync also drains caller streams the device tier ran on
     return enqueue_xfer(gather, TC_XFER_DIRECT, desc, {}, s ? s : s_off);
 }
 

@@ -1,5 +1,5 @@
 // Host runtime of the Tokencake offload/upload hot path: block allocator with per-class partitions, CPU block buffer
-// (pinned host slots), handles, copy streams + events, descriptor ring and the transfer engine.  Internal C++; the C
+// (pinned host slots), handles, copy streams + events, the pinned table-push ring and the transfer engine.  Internal C++; the C
 // ABI in capi.cpp is the only public surface.
 #pragma once
 #include <cuda_runtime.h>
@@ -104,7 +104,7 @@ struct Pool {
     std::vector<cudaEvent_t> events;         // event pool
     std::vector<int32_t> ev_free, ev_used;
 
-    // pinned descriptor / id ring
+    // pinned mapped ring for host->device block-table pushes (decode growth); kernel descriptors travel by value
     char *ring_host = nullptr, *ring_dev = nullptr;
     int64_t ring_cap = 0, ring_head = 0;
 
