@@ -314,15 +314,21 @@ cudaError_t launch_cap(bool gather, const XferDesc *host_desc, int32_t n, const 
     std::copy(host_desc, host_desc + n, dd.d);
     int64_t grid = 0, per = 0;
     if (variant == 1 || variant == 3) {
-        // ring bytes per CTA: 128 KiB, one CTA per SM (1) / 96 KiB, two resident per SM over a 3-per-SM grid, i.e.
-        // 1.5 waves that even out per-channel speed differences (3; profiles/r01_tier_probe_c5_v3.log: 0.98 of the
-        // HBM copy peak at 512 MiB for both 16 KiB and 4 KiB chunks).  stages = ring / piece, so small chunks keep as
-        // many bytes in flight as large ones.
+        // ring bytes per CTA: 128 KiB, one CTA per SM (1) / 96 KiB, two resident per SM (3).  stages = ring / piece,
+        // so small chunks (C5's 4 KiB) keep as many bytes in flight as large ones.  Variant 3's default grid follows
+        // the launch size: ~128 KiB per CTA, between 3 and 15 CTAs per SM — several waves of short CTAs let the block
+        // scheduler even out per-channel speed differences, while a small launch keeps enough work per CTA to fill
+        // its ring (profiles/r01_tier_probe_grid_v4.log: 0.95-1.0 of the HBM copy peak from 100 MiB up, C2 and C5).
         const int32_t piece = (int32_t)std::min<int64_t>(g.chunk, kPieceMax);
         const int64_t K = (int64_t)n * g.two_l * ((g.chunk + piece - 1) / piece);
         const int64_t ring = tma_ring_override() > 0 ? tma_ring_override() : (variant == 1 ? 128 << 10 : 96 << 10);
         const int32_t stages = (int32_t)std::max<int64_t>(2, std::min<int64_t>(kMaxStages, ring / piece));
-        split(K, ctas > 0 ? ctas : (variant == 1 ? 148 : 444), 1, &grid, &per);
+        int64_t want = ctas;
+        if (want <= 0) {
+            const int64_t bytes = (int64_t)n * g.two_l * g.chunk;
+            want = variant == 1 ? 148 : std::max<int64_t>(444, std::min<int64_t>(2220, bytes >> 17));
+        }
+        split(K, want, 1, &grid, &per);
         const size_t smem = (size_t)stages * piece + stages * sizeof(uint64_t);
         auto fn = gather ? k_xfer_bulk<true, kCap> : k_xfer_bulk<false, kCap>;
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
