@@ -34,7 +34,7 @@ from workloads.scripts import CycleGen, setup_ops  # noqa: E402
 METRIC = "KV offload/upload GB/s and blocks/s per GPU vs host-link & HBM peak at 1/2/4/8 GPUs"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 XFER_NAMES = {1: "direct", 2: "staged", 3: "copy"}
-NVLINK_GBS = 900.0      # NVLink 5 per direction per GPU (task statement); only used when a real peer GPU exists
+NVLINK_GBS = 770.0      # peer copy per direction, measured on this pool (B200_PROFILING.md; 900 nominal)
 HBM_FALLBACK = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback (GB/s), only if MEASURED_PEAKS.json is absent
 
 
@@ -348,7 +348,7 @@ def run_ours(args):
              "timing": "kernel-recorded %globaltimer first-CTA start -> last-CTA end, every launch of the timed region"}
         if "peer" in k and not self_peer:   # neighbour's HBM over NVLink: B per block over the link
             e.update(bound="nvlink", achieved=byt / (ms * 1e-3) / 1e9, peak=NVLINK_GBS,
-                     peak_source="NVLink 5 nominal per direction (no measured peak in MEASURED_PEAKS.json)")
+                     peak_source="B200_PROFILING.md measured peer copy, per direction (900 nominal)")
         elif "peer" in k or not link_bound[k]:   # device-side kernel (staged, or a same-GPU peer slab): HBM r+w
             e.update(bound="hbm", achieved=2 * byt / (ms * 1e-3) / 1e9, peak=hbm, peak_source=hbm_src,
                      bytes_per_launch=2 * byt / cnt)
