@@ -355,6 +355,13 @@ tc_status tc_stats(tc_pool *p, tc_stats_t *s) {
 tc_status tc_timing(tc_pool *p, int32_t enable, tc_timing_t *out) {
     TC_GUARD(p) {
         if (enable < 0 || enable > 2) return TC_E_INVAL;
+        if (!P.meta_only && !P.kts_meta.empty()) {     // kernel stamps are collected lazily (runtime.cpp)
+            for (cudaStream_t s : {P.s_up, P.s_off, P.s_up_k, P.s_off_k})
+                if (cudaStreamSynchronize(s) != cudaSuccess) return P.cuda_fail(cudaGetLastError(), "timing sync");
+            for (cudaStream_t f : P.foreign)
+                if (cudaStreamSynchronize(f) != cudaSuccess) return P.cuda_fail(cudaGetLastError(), "timing sync");
+            P.stamps_collect();
+        }
         P.timing = P.meta_only ? 0 : enable;
         if (out) {
             *out = P.tacc;

@@ -316,7 +316,13 @@ void Pool::spans_collect() {
         tev_free.push_back(sp.b);
     }
     spans.clear();
-    if (!kts_meta.empty()) {                        // device-side kernel durations (%globaltimer)
+}
+
+// Device-side kernel durations (%globaltimer stamps) of the launches since the last collection.  Deferred: called by
+// tc_timing() and by tc_sync only when the stamp buffer is nearly full, so a sync costs no extra copies while
+// timing mode 2 runs (the bench's timed region).  Callers have drained the streams.
+void Pool::stamps_collect() {
+    if (!kts_meta.empty()) {
         const size_t used = kts_meta.size();
         std::vector<unsigned long long> buf(2 * used);
         if (cudaMemcpy(buf.data(), kts_dev, used * 16, cudaMemcpyDeviceToHost) == cudaSuccess) {
@@ -1192,6 +1198,7 @@ tc_status Pool::sync() {
         TC_CUDA(cudaStreamSynchronize(s_off_k), "sync offload aux stream");
         for (cudaStream_t f : foreign) TC_CUDA(cudaStreamSynchronize(f), "sync caller stream");
         spans_collect();
+        if ((int64_t)kts_meta.size() > kKts / 2) stamps_collect();
         ++sync_count;
     }
     for (auto &pc : pending_dev) {        // a4 retire in issue order (A10)

@@ -144,10 +144,11 @@ struct Pool {
     tc_status span_begin(cudaStream_t s, cudaEvent_t *a);
     tc_status span_end(cudaStream_t s, int32_t kind, cudaEvent_t a, int64_t bytes, bool link = true);
     void spans_collect();
+    void stamps_collect();
     std::vector<tc_span_t> timeline;         // per-span records (tc_timeline), capped
     int64_t timeline_cap = 0;
     int64_t sync_count = 0;
-    static constexpr int64_t kKts = 4096;    // timed launches per sync interval
+    static constexpr int64_t kKts = 65536;   // kernel stamp slots between collections
     unsigned long long *kts_dev = nullptr;   // device {start, end} %globaltimer pairs, one per timed launch
     std::vector<unsigned long long> kts_init;
     std::vector<std::pair<int32_t, int64_t>> kts_meta;   // (kind, bytes) per used pair
