@@ -231,7 +231,7 @@ def run_ours(args):
                 uoff = np.zeros(len(hs) + 1, dtype=np.int64)
                 uoff[1:] = np.cumsum([sizes.pop(int(h)) for h in hs])
                 ags = np.array([a for a, _ in op[2]], dtype=np.int32)
-                tabs = [np.asarray(pool.block_table(int(a)), dtype=np.int32) for a in ags]
+                tabs = [pool.block_table_np(int(a)) for a in ags]
                 tabs = [t[t >= 0] for t in tabs]
                 ooff = np.zeros(len(tabs) + 1, dtype=np.int64)
                 ooff[1:] = np.cumsum([len(t) for t in tabs])

@@ -350,11 +350,15 @@ class Pool:
         self._check(lib.tc_stream_wait(self._h, h, stream_ptr))
 
     def block_table(self, agent: int) -> list:
+        return self.block_table_np(agent).tolist()
+
+    def block_table_np(self, agent: int) -> np.ndarray:
+        """The agent's block table as an int32 array (-1 = on host): one tc_block_table call into a row-sized
+        buffer (the hot-loop form)."""
         n = ctypes.c_int64()
-        self._check(lib.tc_block_table(self._h, agent, None, 0, ctypes.byref(n)))
-        out = np.empty(max(n.value, 1), dtype=np.int32)
+        out = np.empty(self.max_bpa, dtype=np.int32)
         self._check(lib.tc_block_table(self._h, agent, _ptr(out, ctypes.c_int32), out.size, ctypes.byref(n)))
-        return out[:n.value].tolist()
+        return out[:n.value]
 
     def handle_info(self, h: int):
         a, n, s = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int32()

@@ -59,15 +59,17 @@ __device__ __forceinline__ void st_stream(int4 *p, const int4 &v) {
                  : "memory");
 }
 
-// Device-side launch timing (tc_timing): earliest CTA start / latest CTA end on the %globaltimer clock (ns), so a
-// kernel's duration excludes host launch latency.  g.ts = {start, end}, pre-set to {UINT64_MAX, 0}; null = off.
+// Device-side launch timing (tc_timing): CTA 0's start (CTAs are dispatched in index order, so it is the first) and
+// the latest CTA end on the %globaltimer clock (ns), so a kernel's duration excludes host launch latency.  Only CTA 0
+// stamps the start: thousands of same-address atomics at launch would serialise at one L2 slice and delay the first
+// loads by microseconds.  g.ts = {start, end}, pre-set to {UINT64_MAX, 0}; null = off.
 __device__ __forceinline__ unsigned long long now_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
 __device__ __forceinline__ void ts_begin(const XferGeom &g) {
-    if (g.ts) atomicMin(g.ts, now_ns());
+    if (g.ts && blockIdx.x == 0) atomicMin(g.ts, now_ns());
 }
 __device__ __forceinline__ void ts_end(const XferGeom &g) {
     if (g.ts) atomicMax(g.ts + 1, now_ns());
