@@ -6,9 +6,26 @@
 #include <cstring>
 #include <new>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "runtime.hpp"
 
 using tc::Pool;
+
+// Mutating entry points: an NVTX range named after the call (visible in Nsight Systems / ncu), and with TC_CHECK=1
+// the SPEC invariants re-checked after the call (Pool::check_invariants).
+namespace {
+struct Mut {
+    const Pool &p;
+    const char *name;
+    Mut(const Pool &p_, const char *n) : p(p_), name(n) { nvtxRangePushA(n); }
+    ~Mut() {
+        nvtxRangePop();
+        if (p.check) p.check_invariants(name);
+    }
+};
+}  // namespace
+#define TC_MUT(name) Mut mut_(P, name)
 
 #define TC_GUARD(p)                         \
     if (!(p)) return TC_E_INVAL;            \
@@ -130,31 +147,44 @@ tc_status tc_fill_kv(tc_pool *p, uint64_t seed) {
 }
 
 tc_status tc_partition_reserve(tc_pool *p, int32_t agent_class, int64_t n_blocks) {
-    TC_GUARD(p) { return P.reserve(agent_class, n_blocks); }
+    TC_GUARD(p) {
+        TC_MUT("tc_partition_reserve");
+        return P.reserve(agent_class, n_blocks);
+    }
     TC_CATCH
 }
 
 tc_status tc_agent_add(tc_pool *p, int32_t agent, int32_t agent_class) {
-    TC_GUARD(p) { return P.agent_add(agent, agent_class); }
+    TC_GUARD(p) {
+        TC_MUT("tc_agent_add");
+        return P.agent_add(agent, agent_class);
+    }
     TC_CATCH
 }
 
 tc_status tc_alloc(tc_pool *p, int32_t agent, int64_t n, int32_t *out_ids) {
     TC_GUARD(p) {
         if (!out_ids) return TC_E_INVAL;
+        TC_MUT("tc_alloc");
         return P.alloc_blocks(agent, n, out_ids);
     }
     TC_CATCH
 }
 
 tc_status tc_agent_free(tc_pool *p, int32_t agent) {
-    TC_GUARD(p) { return P.agent_free(agent); }
+    TC_GUARD(p) {
+        TC_MUT("tc_agent_free");
+        return P.agent_free(agent);
+    }
     TC_CATCH
 }
 
 tc_status tc_offload(tc_pool *p, int32_t agent, const int32_t *block_ids, int64_t n, tc_handle *out) {
     const int64_t off[2] = {0, n};
-    TC_GUARD(p) { return P.offload_batch(1, &agent, off, block_ids, out); }
+    TC_GUARD(p) {
+        TC_MUT("tc_offload");
+        return P.offload_batch(1, &agent, off, block_ids, out);
+    }
     TC_CATCH
 }
 
@@ -163,6 +193,7 @@ tc_status tc_upload(tc_pool *p, tc_handle h, int32_t *out_new_ids) {
         auto it = P.handles.find(h);
         if (it == P.handles.end() || it->second.state != tc::kOffloaded) return TC_E_HANDLE;
         const int64_t off[2] = {0, (int64_t)it->second.pos.size()};
+        TC_MUT("tc_upload");
         return P.upload_batch(1, &h, off, out_new_ids);
     }
     TC_CATCH
@@ -170,13 +201,19 @@ tc_status tc_upload(tc_pool *p, tc_handle h, int32_t *out_new_ids) {
 
 tc_status tc_offload_batch(tc_pool *p, int32_t n_agents, const int32_t *agents, const int64_t *offsets,
                            const int32_t *block_ids, tc_handle *out_handles) {
-    TC_GUARD(p) { return P.offload_batch(n_agents, agents, offsets, block_ids, out_handles); }
+    TC_GUARD(p) {
+        TC_MUT("tc_offload_batch");
+        return P.offload_batch(n_agents, agents, offsets, block_ids, out_handles);
+    }
     TC_CATCH
 }
 
 tc_status tc_upload_batch(tc_pool *p, int32_t n_handles, const tc_handle *hs, const int64_t *offsets,
                           int32_t *out_new_ids) {
-    TC_GUARD(p) { return P.upload_batch(n_handles, hs, offsets, out_new_ids); }
+    TC_GUARD(p) {
+        TC_MUT("tc_upload_batch");
+        return P.upload_batch(n_handles, hs, offsets, out_new_ids);
+    }
     TC_CATCH
 }
 
@@ -184,6 +221,7 @@ tc_status tc_cycle(tc_pool *p, int32_t n_handles, const tc_handle *hs, const int
                    int32_t *out_new_ids, int32_t n_agents, const int32_t *agents, const int64_t *off_offsets,
                    const int32_t *block_ids, tc_handle *out_handles) {
     TC_GUARD(p) {
+        TC_MUT("tc_cycle");
         return P.cycle(n_handles, hs, up_offsets, out_new_ids, n_agents, agents, off_offsets, block_ids,
                        out_handles);
     }
@@ -191,17 +229,26 @@ tc_status tc_cycle(tc_pool *p, int32_t n_handles, const tc_handle *hs, const int
 }
 
 tc_status tc_reserve_begin(tc_pool *p, tc_handle h, int32_t cycles) {
-    TC_GUARD(p) { return P.reserve_begin(h, cycles); }
+    TC_GUARD(p) {
+        TC_MUT("tc_reserve_begin");
+        return P.reserve_begin(h, cycles);
+    }
     TC_CATCH
 }
 
 tc_status tc_reserve_tick(tc_pool *p) {
-    TC_GUARD(p) { return P.reserve_tick(); }
+    TC_GUARD(p) {
+        TC_MUT("tc_reserve_tick");
+        return P.reserve_tick();
+    }
     TC_CATCH
 }
 
 tc_status tc_reserve_cancel(tc_pool *p, tc_handle h) {
-    TC_GUARD(p) { return P.reserve_cancel(h); }
+    TC_GUARD(p) {
+        TC_MUT("tc_reserve_cancel");
+        return P.reserve_cancel(h);
+    }
     TC_CATCH
 }
 
@@ -232,7 +279,10 @@ tc_status tc_stream_wait(tc_pool *p, tc_handle h, void *cuda_stream) {
 }
 
 tc_status tc_sync(tc_pool *p) {
-    TC_GUARD(p) { return P.sync(); }
+    TC_GUARD(p) {
+        TC_MUT("tc_sync");
+        return P.sync();
+    }
     TC_CATCH
 }
 

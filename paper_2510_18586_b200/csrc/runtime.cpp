@@ -156,6 +156,7 @@ tc_status Pool::create(const tc_pool_desc &d) {
     for (int64_t i = 0; i < S; ++i) slots.free_list[i] = S - 1 - i;   // pop() yields 0, 1, 2, ...
     device = d.device;
     meta_only = d.device < 0;
+    check = env_int("TC_CHECK", 0) != 0;
     unbuffered = d.unbuffered != 0;
     next_slot = S;
     mode_d2h = d.xfer_d2h;
@@ -1248,6 +1249,53 @@ tc_status Pool::fill(uint64_t seed) {
     ++n_launch;
     TC_CUDA(cudaStreamSynchronize(s_off), "fill sync");
     return TC_OK;
+}
+
+// TC_CHECK=1 (debug): the SPEC invariants re-derived from scratch after every mutating call;
+// a violation aborts with the failing invariant.  Off by default (O(N) per call).
+void Pool::check_invariants(const char *after) const {
+    auto fail = [&](const char *what) {
+        std::fprintf(stderr, "tokencake invariant violated after %s: %s\n", after, what);
+        std::abort();
+    };
+    int64_t nf = 0, na = 0, np = 0, nr = 0;
+    for (int64_t b = 0; b < N; ++b) {
+        const uint8_t st = alloc.state[b];
+        const bool bit = (alloc.bits[b >> 6] >> (b & 63)) & 1;
+        if (bit != (st == kFree)) fail("free bitmap != block state");
+        nf += st == kFree; na += st == kAlloc; np += st == kPending; nr += st == kReserved;
+    }
+    if (nf + na + np + nr != N) fail("block conservation (S:113)");
+    if (nf != alloc.nfree) fail("free count");
+    if (nr != n_reserved) fail("reserved-block count");
+    int64_t pend = 0;
+    for (const auto &pc : pending_dev) pend += (int64_t)pc.second.size();
+    if (pend != np) fail("pending list != PENDING blocks (P:648)");
+    int64_t owned = 0;
+    for (int32_t a = 0; a < max_agents; ++a) {
+        const AgentRec &ag = agents[a];
+        if (!ag.exists) continue;
+        for (size_t pos = 0; pos < ag.table.size(); ++pos) {
+            const int32_t b = ag.table[pos];
+            if (b < 0) continue;
+            ++owned;
+            if (b >= N || alloc.state[b] != kAlloc || alloc.own_agent[b] != a || alloc.own_pos[b] != (int32_t)pos)
+                fail("table <-> owner bijection");
+        }
+    }
+    if (owned != na) fail("ALLOC blocks not all in tables");
+    for (size_t c = 0; c < alloc.claimed.size(); ++c)
+        if (alloc.claimed[c] < 0) fail("negative claim");
+    if (!unbuffered) {
+        int64_t host_in_use = 0, peer_in_use = 0, rel_host = 0, rel_peer = 0;
+        for (const auto &kv : handles) {
+            if (kv.second.state != kOffloaded) continue;
+            for (int64_t s : kv.second.slots) (is_peer(s) ? peer_in_use : host_in_use) += 1;
+        }
+        for (int64_t s : slots.released) (is_peer(s) ? rel_peer : rel_host) += 1;
+        if ((int64_t)slots.free_list.size() + host_in_use + rel_host != slots.count) fail("host slot conservation");
+        if ((int64_t)peer.free_list.size() + peer_in_use + rel_peer != peer.count) fail("peer slot conservation");
+    }
 }
 
 tc_status Pool::device_tier(bool gather, const int32_t *ids, int64_t n, void *ext, cudaStream_t s) {

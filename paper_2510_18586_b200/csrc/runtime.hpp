@@ -144,6 +144,8 @@ struct Pool {
     tc_status span_begin(cudaStream_t s, cudaEvent_t *a);
     tc_status span_end(cudaStream_t s, int32_t kind, cudaEvent_t a, int64_t bytes, bool link = true);
     void spans_collect();
+    bool check = false;                      // TC_CHECK=1: invariants after every mutating call
+    void check_invariants(const char *after) const;
     void stamps_collect();
     std::vector<tc_span_t> timeline;         // per-span records (tc_timeline), capped
     int64_t timeline_cap = 0;

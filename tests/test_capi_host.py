@@ -174,3 +174,23 @@ def test_create_rejects_bad_geometry():
         with pytest.raises(tcb.TcError) as e:
             tcb.Pool(args["L"], args["H"], args["D"], 16, "fp16", 8, device=-1, shard_world=2 if kw.get("H") else 1)
         assert e.value.status == tcb.E_INVAL
+
+
+def test_randomized_safety_suite_1e5_events_with_invariant_checks(monkeypatch):
+    """S:606 randomized safety suite: 10^5 events (20 scripts x 5000 ops, peer tier and gradual reservation on) through
+    the C ABI with TC_CHECK=1 — the library re-derives every SPEC invariant after each mutating call and aborts on a
+    violation — while matching the oracle's statuses, ids and tables op by op."""
+    monkeypatch.setenv("TC_CHECK", "1")
+    total = 0
+    for seed in range(20):
+        rng = np.random.default_rng(seed)
+        N, S, P = 48, int(rng.choice([4, 12])), int(rng.choice([0, 6]))
+        ops = fuzz_script(9000 + seed, n_ops=5000, n_agents=4, n_classes=2, N=N, max_alloc=6, gradual=seed % 2 == 0)
+        o = OraclePool(N, S, n_classes=2, max_agents=1024, store=ProvStore(N, S + P), n_peer_slots=P)
+        c = meta_pool(N, S, ncls=2, P=P)
+        ro, rc = Replayer(o), Replayer(c)
+        for i, op in enumerate(ops):
+            assert ro.step(op) == rc.step(op), (seed, i, op)
+        assert stats_view(o.stats()) == stats_view(c.stats())
+        total += len(ops)
+    assert total >= 100_000
