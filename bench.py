@@ -417,7 +417,7 @@ def run_ours(args):
         "memcpy_calls_per_step": (stats["memcpy_calls"] - memcpy0) / n_steps,
         "kernels": kern,
         "sm_time_share": {
-            "value": sum(v["ms_total"] for k, v in kern.items() if k.endswith("_kernel")) / dev_total_ms,
+            "value": sum(v["ms_total"] for k, v in kern.items() if k.endswith("_kernel")) / sum(dev_ms),
             "how": "sum of the transfer kernels' device durations / the steps' device time: the fraction of the step "
                    "during which this path occupies SMs (the copy-engine DMAs use none); rank 0"},
         "timeline": tl_summary,
