@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--peer", action="store_true",
                     help="NEXT-2 peer tier: as many peer slots as host slots, in the next GPU's HBM (this GPU's own "
                          "HBM when it is alone); offloads go there first")
+    ap.add_argument("--trace", default=None, metavar="FILE",
+                    help="write the per-call trace (tc_trace) of the diagnostic steps as JSONL")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--quick", action="store_true", help="skip host-link probe and device-tier microbench")
@@ -301,9 +303,15 @@ def run_ours(args):
     pool.timing(1)
     pool.timing(1)
     pool.timeline_arm(200000)
+    if args.trace:
+        pool.trace(100000)
     n_diag = min(args.steps, 20)
     for _ in range(n_diag):
         cycle()
+    if args.trace and rank == 0:
+        with open(args.trace, "w") as f:
+            for r in pool.trace_read(100000):
+                f.write(json.dumps(r) + "\n")
     diag = pool.timing(0)
     tl_raw = pool.timeline(200000)
     tl_summary = timeline_summary(tl_raw)

@@ -240,6 +240,20 @@ typedef struct tc_span_t {
     int64_t bytes;
 } tc_span_t;
 tc_status tc_timeline(tc_pool *p, int64_t cap, tc_span_t *out, int64_t *n_out);
+/* Per-call trace (SPEC S:298 trace events offload_done / upload_done with timestamps and block counts):
+   one record per offloaded or uploaded handle — op (1 offload, 2 upload), agent, handle, blocks, bytes (n * B), and
+   host steady-clock nanoseconds at the call's entry, when its GPU work was enqueued, and when that work completed (a
+   cudaLaunchHostFunc callback on the direction's stream; 0 until then; = enqueued on a metadata-only pool).
+   tc_trace(p, cap): cap > 0 arms recording of up to cap records (clearing old ones), cap = 0 turns it off.
+   tc_trace_read copies up to cap records (call tc_sync first for complete t_done) and clears them. */
+typedef struct tc_trace_t {
+    int32_t op, agent;
+    uint64_t handle;
+    int64_t blocks, bytes;
+    int64_t t_call_ns, t_enqueued_ns, t_done_ns;
+} tc_trace_t;
+tc_status tc_trace(tc_pool *p, int64_t cap);
+tc_status tc_trace_read(tc_pool *p, tc_trace_t *out, int64_t cap, int64_t *n_out);
 const char *tc_strerror(tc_status s);
 const char *tc_last_error(tc_pool *p);
 

@@ -30,7 +30,7 @@ SYMBOLS = [
     "tc_agent_add", "tc_alloc", "tc_agent_free", "tc_offload", "tc_upload", "tc_offload_batch", "tc_upload_batch",
     "tc_cycle", "tc_reserve_begin", "tc_reserve_tick", "tc_reserve_cancel", "tc_reserve_info",
     "tc_query", "tc_wait", "tc_stream_wait", "tc_sync", "tc_block_table", "tc_block_table_dev", "tc_handle_info",
-    "tc_handle_host", "tc_handle_read", "tc_stats", "tc_timing", "tc_timeline", "tc_strerror", "tc_last_error", "tc_gather_dev",
+    "tc_handle_host", "tc_handle_read", "tc_stats", "tc_timing", "tc_timeline", "tc_trace", "tc_trace_read", "tc_strerror", "tc_last_error", "tc_gather_dev",
     "tc_scatter_dev",
     # decision layers (paper_2510_18586_b200/sched.py binds them)
     "tc_fc_predict", "tc_fc_observe", "tc_transfer_ms", "tc_xfer_model_measure", "tc_should_offload",
@@ -62,6 +62,12 @@ class Timing(ctypes.Structure):
     _fields_ = [("ms", ctypes.c_double * 9), ("count", ctypes.c_int64 * 9), ("bytes", ctypes.c_int64 * 9),
                 ("kernel_ms", ctypes.c_double * 9), ("kernel_count", ctypes.c_int64 * 9),
                 ("kernel_bytes", ctypes.c_int64 * 9)]
+
+
+class TraceRec(ctypes.Structure):
+    _fields_ = [("op", ctypes.c_int32), ("agent", ctypes.c_int32), ("handle", ctypes.c_uint64),
+                ("blocks", ctypes.c_int64), ("bytes", ctypes.c_int64), ("t_call_ns", ctypes.c_int64),
+                ("t_enqueued_ns", ctypes.c_int64), ("t_done_ns", ctypes.c_int64)]
 
 
 class Span(ctypes.Structure):
@@ -130,6 +136,8 @@ def _load() -> ctypes.CDLL:
         "tc_stats": (I32, [P, ctypes.POINTER(Stats)]),
         "tc_timing": (I32, [P, I32, ctypes.POINTER(Timing)]),
         "tc_timeline": (I32, [P, I64, ctypes.POINTER(Span), PI64]),
+        "tc_trace": (I32, [P, I64]),
+        "tc_trace_read": (I32, [P, ctypes.POINTER(TraceRec), I64, PI64]),
         "tc_strerror": (ctypes.c_char_p, [I32]),
         "tc_last_error": (ctypes.c_char_p, [P]),
         "tc_gather_dev": (I32, [P, PI32, I64, VP, VP]),
@@ -398,6 +406,20 @@ class Pool:
         for i in KERNEL_KINDS:
             out["dev_" + TIMING_KINDS[i]] = (t.kernel_ms[i], t.kernel_count[i], t.kernel_bytes[i])
         return out
+
+    def trace(self, cap: int = 100000):
+        """Arm (cap > 0) or stop (0) the per-call trace (tc_trace)."""
+        self._check(lib.tc_trace(self._h, cap))
+
+    def trace_read(self, cap: int = 100000) -> list:
+        """Per-call records since the last read: dicts with op ('offload' | 'upload'), agent, handle, blocks, bytes,
+        t_call_ns, t_enqueued_ns, t_done_ns (host steady clock)."""
+        buf = (TraceRec * cap)()
+        n = ctypes.c_int64()
+        self._check(lib.tc_trace_read(self._h, buf, cap, ctypes.byref(n)))
+        ops = {1: "offload", 2: "upload"}
+        return [{"op": ops[buf[i].op], **{k: getattr(buf[i], k) for k, _ in TraceRec._fields_ if k != "op"}}
+                for i in range(n.value)]
 
     def timeline_arm(self, cap: int = 100000):
         n = ctypes.c_int64()

@@ -422,6 +422,41 @@ tc_status tc_timing(tc_pool *p, int32_t enable, tc_timing_t *out) {
     TC_CATCH
 }
 
+// Drain every stream the pool uses (trace records are written by host callbacks queued on them).
+static tc_status drain(Pool &P) {
+    if (P.meta_only) return TC_OK;
+    for (cudaStream_t s : {P.s_up, P.s_off, P.s_up_k, P.s_off_k})
+        if (cudaStreamSynchronize(s) != cudaSuccess) return P.cuda_fail(cudaGetLastError(), "drain");
+    return TC_OK;
+}
+
+tc_status tc_trace(tc_pool *p, int64_t cap) {
+    TC_GUARD(p) {
+        if (cap < 0) return TC_E_INVAL;
+        const tc_status st = drain(P);
+        if (st != TC_OK) return st;
+        P.trace_buf.reset(cap > 0 ? new tc_trace_t[cap] : nullptr);
+        P.trace_cap = cap;
+        P.trace_n = 0;
+        return TC_OK;
+    }
+    TC_CATCH
+}
+
+tc_status tc_trace_read(tc_pool *p, tc_trace_t *out, int64_t cap, int64_t *n_out) {
+    TC_GUARD(p) {
+        if (!out || !n_out || cap < 0) return TC_E_INVAL;
+        const tc_status st = drain(P);
+        if (st != TC_OK) return st;
+        const int64_t n = std::min(cap, P.trace_n);
+        if (n > 0) std::memcpy(out, P.trace_buf.get(), (size_t)n * sizeof(tc_trace_t));
+        *n_out = n;
+        P.trace_n = 0;
+        return TC_OK;
+    }
+    TC_CATCH
+}
+
 tc_status tc_timeline(tc_pool *p, int64_t cap, tc_span_t *out, int64_t *n_out) {
     TC_GUARD(p) {
         if (!n_out) return TC_E_INVAL;

@@ -70,6 +70,11 @@ void BlockAllocator::set_free(int32_t b) {
     if ((b >> 6) < hint) hint = b >> 6;
 }
 
+static int64_t steady_ns() {
+    return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
 // ------------------------------------------------------------------------------------------------ host trace
 // TC_HOST_TRACE=1: per tc_cycle, the host time (µs from the call's entry) at which each enqueue step returned, on
 // stderr.  A debugging aid for the enqueue critical path (how soon each link direction gets its first DMA).
@@ -1010,6 +1015,7 @@ void Pool::commit_upload(const UpPlan &P, int32_t ev, int32_t *out_ids) {
 tc_status Pool::offload_batch(int32_t na, const int32_t *ags, const int64_t *off, const int32_t *ids,
                               tc_handle *out) {
     if (cuda_dead) return TC_E_CUDA;
+    if (trace_cap > 0) trace_t0 = steady_ns();
     if (!out) return TC_E_INVAL;
     OffPlan P;
     tc_status st = plan_offload(P, na, ags, off, ids);
@@ -1026,11 +1032,13 @@ tc_status Pool::offload_batch(int32_t na, const int32_t *ags, const int64_t *off
         if ((st = ev_rec(s_off, &ev)) != TC_OK) return st;
     }
     commit_offload(P, ev, out);
+    trace_calls(1, ags, out, off, na, s_off);
     return TC_OK;
 }
 
 tc_status Pool::upload_batch(int32_t nh, const tc_handle *hs, const int64_t *off, int32_t *out_ids) {
     if (cuda_dead) return TC_E_CUDA;
+    if (trace_cap > 0) trace_t0 = steady_ns();
     if (!out_ids) return TC_E_INVAL;
     UpPlan P;
     tc_status st = plan_upload(P, nh, hs, off);
@@ -1047,6 +1055,7 @@ tc_status Pool::upload_batch(int32_t nh, const tc_handle *hs, const int64_t *off
         if ((st = ev_rec(s_up, &ev)) != TC_OK) return st;
     }
     commit_upload(P, ev, out_ids);
+    trace_calls(2, nullptr, hs, off, nh, s_up);
     return TC_OK;
 }
 
@@ -1058,6 +1067,7 @@ tc_status Pool::cycle(int32_t nh, const tc_handle *hs, const int64_t *up_off, in
                       const int32_t *ags, const int64_t *off_off, const int32_t *ids, tc_handle *out_h) {
     if (cuda_dead) return TC_E_CUDA;
     if (nh < 0 || na < 0 || (nh > 0 && !out_ids) || (na > 0 && !out_h)) return TC_E_INVAL;
+    if (trace_cap > 0) trace_t0 = steady_ns();
     if (g_trace) {
         g_trace_t0 = std::chrono::steady_clock::now();
         g_trace_buf = "[tc trace] cycle";
@@ -1100,6 +1110,8 @@ tc_status Pool::cycle(int32_t nh, const tc_handle *hs, const int64_t *up_off, in
     }
     if (nh > 0) commit_upload(U, ev_up, out_ids);
     if (na > 0) commit_offload(O, ev_off, out_h);
+    if (nh > 0) trace_calls(2, nullptr, hs, up_off, nh, s_up);
+    if (na > 0) trace_calls(1, ags, out_h, off_off, na, s_off);
     if (g_trace) {
         trace("commit");
         std::fprintf(stderr, "%s\n", g_trace_buf.c_str());
@@ -1249,6 +1261,28 @@ tc_status Pool::fill(uint64_t seed) {
     ++n_launch;
     TC_CUDA(cudaStreamSynchronize(s_off), "fill sync");
     return TC_OK;
+}
+
+// ------------------------------------------------------------------------------------------------ per-call trace
+static void CUDART_CB trace_done(void *rec) {
+    reinterpret_cast<tc_trace_t *>(rec)->t_done_ns = steady_ns();
+}
+
+// One record per handle of a just-enqueued batch; their completion is stamped by a host callback queued on `s`
+// behind the batch's work (so t_done - t_enqueued is the transfer as the host sees it).
+void Pool::trace_calls(int32_t op, const int32_t *ags, const tc_handle *hs, const int64_t *off, int32_t k,
+                       cudaStream_t s) {
+    if (trace_cap <= 0) return;
+    const int64_t t_enq = steady_ns();
+    for (int32_t i = 0; i < k && trace_n < trace_cap; ++i) {
+        tc_trace_t &r = trace_buf[trace_n++];
+        const int64_t nb = off[i + 1] - off[i];
+        r = tc_trace_t{op, ags ? ags[i] : handles.at(hs[i]).agent, hs[i], nb, nb * B, trace_t0, t_enq, 0};
+        if (meta_only || cudaLaunchHostFunc(s, trace_done, &r) != cudaSuccess) {
+            cudaGetLastError();
+            r.t_done_ns = t_enq;
+        }
+    }
 }
 
 // TC_CHECK=1 (debug): the SPEC invariants re-derived from scratch after every mutating call;

@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <map>
+#include <memory>
 #include <set>
 #include <string>
 #include <unordered_map>
@@ -148,6 +149,12 @@ struct Pool {
     void check_invariants(const char *after) const;
     void stamps_collect();
     std::vector<tc_span_t> timeline;         // per-span records (tc_timeline), capped
+    // per-call trace (tc_trace): records live in a fixed array so the completion callbacks can fill t_done in place
+    std::unique_ptr<tc_trace_t[]> trace_buf;
+    int64_t trace_cap = 0, trace_n = 0;
+    int64_t trace_t0 = 0;                    // t_call of the call being enqueued
+    void trace_calls(int32_t op, const int32_t *agents, const tc_handle *hs, const int64_t *off, int32_t k,
+                     cudaStream_t s);
     int64_t timeline_cap = 0;
     int64_t sync_count = 0;
     static constexpr int64_t kKts = 65536;   // kernel stamp slots between collections

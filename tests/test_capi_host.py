@@ -194,3 +194,32 @@ def test_randomized_safety_suite_1e5_events_with_invariant_checks(monkeypatch):
         assert stats_view(o.stats()) == stats_view(c.stats())
         total += len(ops)
     assert total >= 100_000
+
+
+def test_per_call_trace_records():
+    """tc_trace (SURVEY.md §5 tracing; SPEC S:298 offload_done / upload_done with block counts): one record per handle
+    per offload / upload, in call order, with monotone host timestamps; a metadata-only pool stamps completion at
+    enqueue.  tc_trace(0) stops recording; bad arguments -> INVAL."""
+    c = meta_pool(32, 8)
+    c.trace(16)
+    c.agent_add(0, 0)
+    c.agent_add(1, 1)
+    a = c.alloc(0, 3)
+    b = c.alloc(1, 2)
+    hs = c.offload_batch([(0, list(a)), (1, list(b))])
+    c.sync()
+    c.upload_batch(hs)
+    c.sync()
+    recs = c.trace_read()
+    assert [(r["op"], r["agent"], r["handle"], r["blocks"]) for r in recs] == \
+        [("offload", 0, hs[0], 3), ("offload", 1, hs[1], 2), ("upload", 0, hs[0], 3), ("upload", 1, hs[1], 2)]
+    for r in recs:
+        assert r["bytes"] == r["blocks"] * c.block_bytes
+        assert r["t_call_ns"] <= r["t_enqueued_ns"] == r["t_done_ns"]
+    assert c.trace_read() == []
+    c.trace(0)
+    h = c.offload(0, c.block_table(0))
+    assert c.trace_read() == [] and h
+    with pytest.raises(tcb.TcError) as e:
+        c.trace(-1)
+    assert e.value.status == tcb.E_INVAL

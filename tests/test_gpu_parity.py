@@ -335,3 +335,19 @@ def test_head_shards_concatenate_to_unsharded_run():
             assert p.block_table(a) == pools[0][0].block_table(a)
     for p, _ in pools:
         p.close()
+
+
+def test_per_call_trace_completion_stamps():
+    """On the GPU the trace's t_done comes from a host callback behind the batch's work: after tc_sync every record
+    has t_call <= t_enqueued <= t_done."""
+    L, H, D, N, S = 2, 2, 64, 64, 32
+    c = dev_pool(L, H, D, N, S, "staged")
+    c.trace(64)
+    r = Replayer(c)
+    r.run(fuzz_script(3, n_ops=60, n_agents=3, n_classes=2, N=N, max_alloc=6))
+    c.sync()
+    recs = c.trace_read()
+    assert recs and {x["op"] for x in recs} == {"offload", "upload"}
+    for x in recs:
+        assert 0 < x["t_call_ns"] <= x["t_enqueued_ns"] <= x["t_done_ns"], x
+    c.close()
