@@ -294,6 +294,8 @@ def run_ours(args):
         bytes_off += no * B
         blocks += nu + no
     torch.cuda.synchronize(dev)
+    if dist is not None:
+        dist.barrier()
     t_wall = time.perf_counter() - t_wall0
     clk = clocks.stop()
     tim = pool.timing(0)
