@@ -1,0 +1,55 @@
+"""CPU checks of bench.py's host-side pieces: workload selection and scaling labels per config, the per-step timeline
+summary, the ncu-traffic lookup, and the reference (oracle) arm's JSON line contract."""
+import json
+import os
+import subprocess
+import sys
+from types import SimpleNamespace
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+
+
+@pytest.mark.parametrize("name,world,G,scaling", [("c2", 1, 1, "weak"), ("c2", 8, 1, "weak"), ("c3", 4, 1, "weak"),
+                                                  ("c4", 1, 1, "weak"), ("c4", 8, 8, "strong"),
+                                                  ("c5", 1, 8, "weak"), ("c5", 2, 8, "weak")])
+def test_workload_for(name, world, G, scaling):
+    cfg, g, sc = bench.workload_for(SimpleNamespace(workload=name), world)
+    assert (cfg.name, g, sc) == (name, G, scaling)
+
+
+def test_timeline_summary():
+    spans = [(0, "memcpy_h2d", 0.0, 2.0, 10), (0, "memcpy_d2h", 0.1, 2.5, 10), (0, "offload_kernel", 0.01, 0.05, 10),
+             (1, "memcpy_h2d", 0.0, 1.0, 10), (1, "memcpy_d2h", 0.3, 1.5, 10)]
+    s = bench.timeline_summary(spans)
+    assert s["steps"] == 2
+    assert s["step_span_ms"] == pytest.approx((2.5 + 1.5) / 2)
+    assert s["d2h_start_ms"] == pytest.approx(0.2)
+    assert s["tail_after_last_dma_ms"] == pytest.approx(0.0)
+    assert bench.timeline_summary([]) is None
+
+
+def test_ncu_traffic_lookup():
+    kd = {"bound": "hbm", "bytes_per_launch": 1000.0}
+    t = bench.ncu_traffic("c2", "gather", kd)
+    if os.path.exists(os.path.join(ROOT, "profiles", "r01_traffic_c2.json")):
+        assert 0.5 < t["traffic_source"]["dram_over_algorithmic"] < 1.5
+        assert t["traffic"] == pytest.approx(1000.0 * t["traffic_source"]["dram_over_algorithmic"])
+        assert abs(t["traffic_source"]["dram_read_over_algorithmic_read"] - 1.0) < 0.01
+    assert bench.ncu_traffic("c2", "gather", {"bound": "host_link", "bytes_per_launch": 1.0}) == {}
+    assert bench.ncu_traffic("nosuch", "gather", kd) == {}
+
+
+def test_reference_arm_json_line():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr
+    lines = [ln for ln in out.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["unit"] == "GB/s" and d["higher_is_better"] is True
+    assert d["metric"] == bench.METRIC and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
