@@ -183,13 +183,20 @@ def run_ours(args):
     import paper_2510_18586_b200 as tcb
 
     rank, world, local = dist_env()
+    # TC_BENCH_DEVICE / TC_BENCH_BACKEND=gloo: rehearse the N-rank flow with every rank on one GPU (a box with a
+    # single GPU cannot run NCCL between ranks sharing it); the timing numbers of such a run are not a scaling result
+    local = int(os.environ.get("TC_BENCH_DEVICE", local))
+    backend = os.environ.get("TC_BENCH_BACKEND", "nccl")
     numa = bind_numa_local(local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     cfg, G, scaling = workload_for(args, world)
     shard_rank = rank % G if G > 1 else 0
     mode_d2h, mode_h2d = {"auto": (tcb.XFER_AUTO,) * 2, "direct": (tcb.XFER_DIRECT,) * 2,
@@ -322,7 +329,7 @@ def run_ours(args):
             json.dump(tl_raw, f)
 
     my = torch.tensor([sum(dev_ms), sum(host_ms), bytes_up + bytes_off, blocks, t_wall], dtype=torch.float64,
-                      device=dev)
+                      device=dev if backend == "nccl" else "cpu")
     tot = my.clone()
     if dist is not None:
         mx = my.clone(); dist.all_reduce(mx, op=dist.ReduceOp.MAX)
