@@ -223,3 +223,23 @@ def test_per_call_trace_records():
     with pytest.raises(tcb.TcError) as e:
         c.trace(-1)
     assert e.value.status == tcb.E_INVAL
+
+
+def test_header_is_plain_c_and_demo_runs(tmp_path):
+    """The boundary is a C ABI: include/tokencake.h compiles as strict C11 (-pedantic -Werror) and
+    examples/c_abi_demo.c, linked against libtokencake.so, drives offload / upload / block-table remap on a
+    metadata-only pool."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no gcc")
+    exe = tmp_path / "c_abi_demo"
+    libdir = os.path.dirname(tcb.LIB_PATH)
+    r = subprocess.run([gcc, "-std=c11", "-pedantic", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "examples", "c_abi_demo.c"), "-L", libdir, "-ltokencake",
+                        f"-Wl,-rpath,{libdir}", "-o", str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.startswith("ok: 48 blocks")

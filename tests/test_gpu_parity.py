@@ -351,3 +351,23 @@ def test_per_call_trace_completion_stamps():
     for x in recs:
         assert 0 < x["t_call_ns"] <= x["t_enqueued_ns"] <= x["t_done_ns"], x
     c.close()
+
+
+def test_c_abi_demo_on_device(tmp_path):
+    """examples/c_abi_demo.c (plain C, no Python in the loop) on cuda:0: real KV bytes moved through the C ABI."""
+    import os
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no gcc")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.dirname(tcb.LIB_PATH)
+    exe = tmp_path / "c_abi_demo"
+    r = subprocess.run([gcc, "-std=c11", "-I", os.path.join(root, "include"), os.path.join(root, "examples",
+                        "c_abi_demo.c"), "-L", libdir, "-ltokencake", f"-Wl,-rpath,{libdir}", "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe), "0"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.startswith("ok: 48 blocks")
