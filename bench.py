@@ -212,6 +212,9 @@ def run_ours(args):
                     xfer_d2h=mode_d2h, xfer_h2d=mode_h2d, peer_device=peer_dev, peer_slots=S if args.peer else 0)
     pool.fill(cfg.seed)
     B = pool.block_bytes
+    calibration = None
+    if args.mode == "auto" and os.environ.get("TC_BENCH_CALIBRATE", "1") != "0":
+        calibration = pool.calibrate(256 << 20)   # AUTO re-measured on this box
 
     # setup (untimed): quotas, agents, decode-like interleaved pre-fill — through the C ABI
     ops, agents, _ = setup_ops(cfg)
@@ -433,6 +436,7 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "memcpy_calls_per_step": (stats["memcpy_calls"] - memcpy0) / n_steps,
         "kernels": kern,
+        "auto_calibration": calibration,
         "sm_time_share": {
             "value": sum(v["ms_total"] for k, v in kern.items() if k.endswith("_kernel")) / sum(dev_ms),
             "how": "sum of the transfer kernels' device durations / the steps' device time: the fraction of the step "

@@ -56,8 +56,9 @@ typedef enum {
 } tc_status;
 
 typedef enum {
-    TC_XFER_AUTO = 0,    /* per direction: STAGED, the path measured fastest for the cycle on B200, except that a
-                            batch of <= 2 MiB takes DIRECT (one launch, lower latency) */
+    TC_XFER_AUTO = 0,    /* per direction: STAGED, the path measured fastest for the cycle on B200 (re-measured on
+                            this box by tc_calibrate), except that a batch of <= 2 MiB takes DIRECT (one launch,
+                            lower latency) */
     TC_XFER_DIRECT = 1,  /* one SM kernel reads/writes mapped pinned host memory over the host link */
     TC_XFER_STAGED = 2,  /* TMA gather/scatter to a device staging buffer + batched copy-engine DMA */
     TC_XFER_COPY = 3     /* the copy engine moves each block as one strided DMA (2L rows of C bytes, row pitch N*C in
@@ -127,6 +128,20 @@ tc_status tc_set_compute_stream(tc_pool *p, void *cuda_stream);
 tc_status tc_streams(tc_pool *p, void **upload_stream, void **offload_stream);
 /* Override the transfer mode per direction (tc_xfer_mode) for subsequent calls. */
 tc_status tc_set_xfer_mode(tc_pool *p, int32_t d2h, int32_t h2d);
+/* Measure, on this box, which path AUTO should take (north_star: direct mapped-host writes "chosen against a
+   device-staging path plus cudaMemcpyAsync according to the measured bandwidth"): a full cycle — an offload of
+   probe_bytes (gather) and an upload of probe_bytes (scatter) running concurrently — is timed (best of 3) for each of
+   the four {DIRECT, STAGED} x {DIRECT, STAGED} combinations; AUTO directions then take the fastest combination.
+   Uses pool blocks [0, 2k) and 2k free host slots (k = probe_bytes / B, shrunk to what is free; TC_E_NOHOST if not
+   even 1 + 1 fit): the gathered blocks are only read and the scattered ones receive their own bytes back, so the pool's
+   contents are unchanged — but the caller must not run kernels on the pool meanwhile.  Blocking.
+   gbs[i] = 2 * probe bytes / cycle time for combination i = 2 * (d2h is STAGED) + (h2d is STAGED). */
+typedef struct tc_calibration_t {
+    int32_t d2h, h2d;          /* the chosen modes (what AUTO directions now use) */
+    int64_t probe_bytes;       /* bytes per direction actually probed */
+    double gbs[4];
+} tc_calibration_t;
+tc_status tc_calibrate(tc_pool *p, int64_t probe_bytes, tc_calibration_t *out);
 /* Launch configuration of one kernel path: path 0 = direct D2H gather, 1 = direct H2D scatter, 2 = device-side
    gather/scatter (staged mode and device tier), 3 = peer-tier gather/scatter (NEXT-2).  ctas <= 0 -> default grid;
    threads in {32..256} (SIMT variants);

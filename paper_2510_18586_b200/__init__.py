@@ -26,7 +26,7 @@ DTYPES = {"fp16": FP16, "bf16": BF16}
 
 SYMBOLS = [
     "tc_pool_desc_init", "tc_pool_create", "tc_pool_create_ex", "tc_pool_destroy", "tc_pool_kv",
-    "tc_set_compute_stream", "tc_streams", "tc_set_xfer_mode", "tc_set_launch_config", "tc_fill_kv", "tc_partition_reserve",
+    "tc_set_compute_stream", "tc_streams", "tc_set_xfer_mode", "tc_calibrate", "tc_set_launch_config", "tc_fill_kv", "tc_partition_reserve",
     "tc_agent_add", "tc_alloc", "tc_agent_free", "tc_offload", "tc_upload", "tc_offload_batch", "tc_upload_batch",
     "tc_cycle", "tc_reserve_begin", "tc_reserve_tick", "tc_reserve_cancel", "tc_reserve_info",
     "tc_query", "tc_wait", "tc_stream_wait", "tc_sync", "tc_block_table", "tc_block_table_dev", "tc_handle_info",
@@ -62,6 +62,11 @@ class Timing(ctypes.Structure):
     _fields_ = [("ms", ctypes.c_double * 9), ("count", ctypes.c_int64 * 9), ("bytes", ctypes.c_int64 * 9),
                 ("kernel_ms", ctypes.c_double * 9), ("kernel_count", ctypes.c_int64 * 9),
                 ("kernel_bytes", ctypes.c_int64 * 9)]
+
+
+class Calibration(ctypes.Structure):
+    _fields_ = [("d2h", ctypes.c_int32), ("h2d", ctypes.c_int32), ("probe_bytes", ctypes.c_int64),
+                ("gbs", ctypes.c_double * 4)]
 
 
 class TraceRec(ctypes.Structure):
@@ -109,6 +114,7 @@ def _load() -> ctypes.CDLL:
         "tc_set_compute_stream": (I32, [P, VP]),
         "tc_streams": (I32, [P, ctypes.POINTER(VP), ctypes.POINTER(VP)]),
         "tc_set_xfer_mode": (I32, [P, I32, I32]),
+        "tc_calibrate": (I32, [P, I64, ctypes.POINTER(Calibration)]),
         "tc_set_launch_config": (I32, [P, I32, I32, I32, I32]),
         "tc_fill_kv": (I32, [P, U64]),
         "tc_partition_reserve": (I32, [P, I32, I64]),
@@ -443,6 +449,16 @@ class Pool:
 
     def set_xfer_mode(self, d2h: int, h2d: int):
         self._check(lib.tc_set_xfer_mode(self._h, d2h, h2d))
+
+    def calibrate(self, probe_bytes: int = 256 << 20) -> dict:
+        """tc_calibrate: time a concurrent offload + upload of probe_bytes for each {DIRECT, STAGED} combination and
+        make AUTO directions take the fastest; returns the chosen modes and GB/s per combination."""
+        c = Calibration()
+        self._check(lib.tc_calibrate(self._h, probe_bytes, ctypes.byref(c)))
+        names = {XFER_DIRECT: "direct", XFER_STAGED: "staged"}
+        return {"d2h": names[c.d2h], "h2d": names[c.h2d], "probe_bytes": c.probe_bytes,
+                "gbs": {f"{a}/{b}": c.gbs[2 * i + j] for i, a in enumerate(("direct", "staged"))
+                        for j, b in enumerate(("direct", "staged"))}}
 
     def set_launch_config(self, path: int, ctas: int = 0, threads: int = 256, variant: int = 0):
         """path 0 = direct D2H, 1 = direct H2D, 2 = device-side (staged/device tier); variant 1 = TMA bulk."""

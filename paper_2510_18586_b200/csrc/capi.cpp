@@ -129,6 +129,14 @@ tc_status tc_set_xfer_mode(tc_pool *p, int32_t d2h, int32_t h2d) {
     TC_CATCH
 }
 
+tc_status tc_calibrate(tc_pool *p, int64_t probe_bytes, tc_calibration_t *out) {
+    TC_GUARD(p) {
+        TC_MUT("tc_calibrate");
+        return P.calibrate(probe_bytes, out);
+    }
+    TC_CATCH
+}
+
 tc_status tc_set_launch_config(tc_pool *p, int32_t path, int32_t ctas, int32_t threads, int32_t variant) {
     TC_GUARD(p) {
         if (path < 0 || path > 3 || threads < 32 || threads > 256 || threads % 32 || variant < 0 || variant > 3)

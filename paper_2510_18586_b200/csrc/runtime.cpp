@@ -244,6 +244,8 @@ tc_status Pool::create(const tc_pool_desc &d) {
     // AUTO: the copy-engine staged path measured fastest for full cycles on B200 (profiles/r01_staged_ab.md).
     auto_dir[0] = mode_d2h == TC_XFER_AUTO;
     auto_dir[1] = mode_h2d == TC_XFER_AUTO;
+    auto_choice[0] = env_int("TC_AUTO_D2H", TC_XFER_STAGED);
+    auto_choice[1] = env_int("TC_AUTO_H2D", TC_XFER_STAGED);
     if (auto_dir[0]) mode_d2h = auto_mode(0);
     if (auto_dir[1]) mode_h2d = auto_mode(1);
     auto_direct_bytes = env_int("TC_AUTO_DIRECT_KIB", 2048) * 1024ll;
@@ -466,8 +468,72 @@ tc_status Pool::xfer_init(XferJob &j, bool gather, int32_t mode, const std::vect
 // AUTO: the path measured fastest for a full scheduling cycle on B200 (both directions concurrently).
 // A batch of at most auto_direct_bytes still takes the DIRECT kernel: one launch instead of kernel + DMA, ~5 µs
 // sooner for 1-2 blocks and equal from ~2 MiB up (profiles/r01_sweep_c{2,5}.json).
-int32_t Pool::auto_mode(int dir) const {
-    return env_int(dir == 0 ? "TC_AUTO_D2H" : "TC_AUTO_H2D", TC_XFER_STAGED);
+int32_t Pool::auto_mode(int dir) const { return auto_choice[dir]; }
+
+tc_status Pool::calibrate(int64_t probe_bytes, tc_calibration_t *out) {
+    if (meta_only) return TC_E_NODEV;
+    if (cuda_dead) return TC_E_CUDA;
+    if (probe_bytes <= 0 || !out) return TC_E_INVAL;
+    for (cudaStream_t s : {s_up, s_off, s_up_k, s_off_k}) TC_CUDA(cudaStreamSynchronize(s), "calibrate drain");
+    int64_t k = std::max<int64_t>(1, probe_bytes / B);
+    k = std::min<int64_t>({k, N / 2, (int64_t)slots.free_list.size() / 2});
+    if (k < 1) return TC_E_NOHOST;
+    std::vector<XferDesc> da(k), db(k);
+    std::vector<int64_t> sa(k), sb(k);
+    const size_t top = slots.free_list.size();
+    for (int64_t i = 0; i < k; ++i) {              // A = blocks [0, k) (read), B = [k, 2k) (rewritten with itself)
+        da[i] = XferDesc{(int32_t)i, -1, 0};
+        db[i] = XferDesc{(int32_t)(k + i), -1, 0};
+        sa[i] = slots.free_list[top - 1 - i];
+        sb[i] = slots.free_list[top - 1 - k - i];
+    }
+    const bool saved_auto[2] = {auto_dir[0], auto_dir[1]};
+    auto_dir[0] = auto_dir[1] = false;              // probe sizes exactly as given (no small-batch DIRECT)
+    tc_status st = enqueue_xfer(true, TC_XFER_STAGED, db, sb, s_off);   // B's images, so the scatters restore B
+    cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+    double best[4] = {1e30, 1e30, 1e30, 1e30};
+    const int32_t modes[2] = {TC_XFER_DIRECT, TC_XFER_STAGED};
+    if (st == TC_OK && (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess ||
+                        cudaEventCreate(&e2) != cudaSuccess))
+        st = cuda_fail(cudaErrorMemoryAllocation, "calibrate events");
+    for (int rep = 0; st == TC_OK && rep < 4; ++rep) {
+        for (int c = 0; st == TC_OK && c < 4; ++c) {
+            if (cudaStreamSynchronize(s_off) != cudaSuccess || cudaStreamSynchronize(s_up) != cudaSuccess) {
+                st = cuda_fail(cudaGetLastError(), "calibrate sync");
+                break;
+            }
+            cudaEventRecord(e0, s_off);
+            cudaStreamWaitEvent(s_up, e0, 0);
+            if ((st = enqueue_xfer(true, modes[c >> 1], da, sa, s_off)) != TC_OK) break;
+            if ((st = enqueue_xfer(false, modes[c & 1], db, sb, s_up)) != TC_OK) break;
+            cudaEventRecord(e1, s_off);
+            cudaEventRecord(e2, s_up);
+            float t1 = 0.f, t2 = 0.f;
+            if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventSynchronize(e2) != cudaSuccess ||
+                cudaEventElapsedTime(&t1, e0, e1) != cudaSuccess || cudaEventElapsedTime(&t2, e0, e2) != cudaSuccess) {
+                st = cuda_fail(cudaGetLastError(), "calibrate timing");
+                break;
+            }
+            if (rep > 0) best[c] = std::min(best[c], (double)std::max(t1, t2));   // rep 0 warms every path up
+        }
+    }
+    for (cudaEvent_t e : {e0, e1, e2})
+        if (e) cudaEventDestroy(e);
+    auto_dir[0] = saved_auto[0];
+    auto_dir[1] = saved_auto[1];
+    if (st != TC_OK) return st;
+    int bc = 3;
+    for (int c = 0; c < 4; ++c)
+        if (best[c] < best[bc]) bc = c;
+    auto_choice[0] = modes[bc >> 1];
+    auto_choice[1] = modes[bc & 1];
+    if (auto_dir[0]) mode_d2h = auto_choice[0];
+    if (auto_dir[1]) mode_h2d = auto_choice[1];
+    out->d2h = auto_choice[0];
+    out->h2d = auto_choice[1];
+    out->probe_bytes = k * B;
+    for (int c = 0; c < 4; ++c) out->gbs[c] = 2.0 * (double)(k * B) / (best[c] * 1e-3) / 1e9;
+    return TC_OK;
 }
 
 // COPY mode: one strided DMA per block (2L rows of C bytes; pool row pitch N*C, slot rows packed), all blocks of the

@@ -112,6 +112,8 @@ struct Pool {
     // transfer modes
     int32_t mode_d2h = TC_XFER_DIRECT, mode_h2d = TC_XFER_DIRECT;
     bool auto_dir[2] = {false, false};        // the direction's mode came from AUTO (small batches go DIRECT)
+    int32_t auto_choice[2] = {TC_XFER_STAGED, TC_XFER_STAGED};   // what AUTO resolves to (tc_calibrate)
+    tc_status calibrate(int64_t probe_bytes, tc_calibration_t *out);
     int64_t auto_direct_bytes = 2ll << 20;
     // launch config per path: [0] direct D2H, [1] direct H2D, [2] device tier + staged kernels, [3] peer tier
     int ctas[4] = {0, 0, 0, 0}, nthreads[4] = {256, 256, 256, 256}, variant[4] = {0, 0, 3, 3};

@@ -371,3 +371,30 @@ def test_c_abi_demo_on_device(tmp_path):
     r = subprocess.run([str(exe), "0"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr
     assert r.stdout.startswith("ok: 48 blocks")
+
+
+def test_calibrate_keeps_pool_and_sets_auto():
+    """tc_calibrate times the four {DIRECT, STAGED} cycle combinations on this box; the pool's bytes, tables and
+    counters are unchanged afterwards, AUTO directions take the chosen modes, and a later script still matches the
+    oracle byte for byte."""
+    L, H, D, N, S = 4, 4, 128, 96, 64
+    pool0 = content.pool_bytes(21, L, N, 16, H, D)
+    c = tcb.Pool(L, H, D, 16, "bf16", N, device=0, host_slots=S, n_classes=2)
+    c.fill(21)
+    before = c.stats()
+    cal = c.calibrate(8 << 20)
+    assert cal["probe_bytes"] > 0 and all(v > 0 for v in cal["gbs"].values())
+    assert np.array_equal(c.kv_tensor().cpu().numpy(), pool0)
+    after = c.stats()
+    assert {k: before[k] for k in ("free", "alloc", "host_free", "host_used")} == \
+        {k: after[k] for k in ("free", "alloc", "host_free", "host_used")}
+    names = {tcb.XFER_DIRECT: "direct", tcb.XFER_STAGED: "staged"}
+    assert (names[after["xfer_d2h"]], names[after["xfer_h2d"]]) == (cal["d2h"], cal["h2d"])
+    o = OraclePool(N, S, n_classes=2, store=BytesStore(pool0, S))
+    ro, rc = Replayer(o), Replayer(c)
+    for op in fuzz_script(8, n_ops=80, n_agents=3, n_classes=2, N=N, max_alloc=8):
+        assert ro.step(op) == rc.step(op), op
+    c.sync()
+    o.sync()
+    compare_full(o, c, "after calibrate")
+    c.close()
