@@ -285,7 +285,9 @@ tc_status tc_fc_observe(tc_fc_stat *s, double observed_ms, double beta);
 typedef struct tc_xfer_model { double offload_ms_per_block, upload_ms_per_block, fixed_ms; } tc_xfer_model;
 double tc_transfer_ms(const tc_xfer_model *m, int64_t n_blocks);
 /* Calibrate the model from this pool's own measured transfers (needs tc_timing on and at least one tc_sync after
-   an offload and an upload; TC_E_BUSY otherwise) — replaces SPEC's paper-derived 60 ms / 4096 blocks. */
+   an offload and an upload; TC_E_BUSY otherwise) — replaces SPEC's paper-derived 60 ms / 4096 blocks.  Per
+   direction a least-squares line t = fixed + n * per_block over the link-side spans (through the origin when only
+   one size was seen); fixed_ms = the two directions' intercepts. */
 tc_status tc_xfer_model_measure(tc_pool *p, tc_xfer_model *m);
 typedef struct tc_offload_decision {
     int32_t offload;      /* 1 = offload */

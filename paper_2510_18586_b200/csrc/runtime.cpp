@@ -311,8 +311,12 @@ void Pool::spans_collect() {
             tacc.bytes[sp.kind] += sp.bytes;
             if (sp.link && B > 0) {                             // the host-link side of a transfer
                 const int dir = (sp.kind == 7 || sp.kind == 3) ? 0 : 1;
+                const double nb = (double)(sp.bytes / B);
                 cal_ms[dir] += ms;
                 cal_blocks[dir] += sp.bytes / B;
+                cal_cnt[dir] += 1;
+                cal_nn[dir] += nb * nb;
+                cal_nt[dir] += nb * ms;
             }
             if (timeline.size() < (size_t)timeline_cap) {      // start/end relative to this sync interval's first span
                 float t0 = 0.f;

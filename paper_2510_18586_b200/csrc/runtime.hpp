@@ -164,8 +164,11 @@ struct Pool {
     std::vector<unsigned long long> kts_init;
     std::vector<std::pair<int32_t, int64_t>> kts_meta;   // (kind, bytes) per used pair
     XferGeom geom(int32_t kind, int64_t bytes);
-    double cal_ms[2] = {0, 0};               // link-side transfer time per direction (tc_xfer_model_measure)
+    // link-side transfer spans per direction, for the least-squares fit t = fixed + n * per_block
+    // (tc_xfer_model_measure): sums of 1, n, t, n*n, n*t over the spans
+    double cal_ms[2] = {0, 0};
     int64_t cal_blocks[2] = {0, 0};
+    double cal_cnt[2] = {0, 0}, cal_nn[2] = {0, 0}, cal_nt[2] = {0, 0};
 
     // counters / errors
     int64_t n_launch = 0, n_memcpy = 0, bytes_d2h = 0, bytes_h2d = 0;

@@ -37,9 +37,27 @@ tc_status tc_xfer_model_measure(tc_pool *p, tc_xfer_model *m) {
     if (!p || !m) return TC_E_INVAL;
     const tc::Pool &P = p->impl;
     if (P.cal_blocks[0] <= 0 || P.cal_blocks[1] <= 0) return TC_E_BUSY;  // nothing measured yet (tc_timing on)
-    m->offload_ms_per_block = P.cal_ms[0] / (double)P.cal_blocks[0];
-    m->upload_ms_per_block = P.cal_ms[1] / (double)P.cal_blocks[1];
-    m->fixed_ms = 0.0;
+    // per direction, least squares t = a + b*n over the measured spans ("generally linear"); with a single
+    // distinct size the fit degenerates and the line goes through the origin (a = 0, b = mean ms per block)
+    double per[2], fixed = 0.0;
+    for (int d = 0; d < 2; ++d) {
+        const double c = P.cal_cnt[d], sn = (double)P.cal_blocks[d], st = P.cal_ms[d];
+        const double det = c * P.cal_nn[d] - sn * sn;
+        double b = st / sn, a = 0.0;
+        if (c >= 2 && det > 1e-9 * c * P.cal_nn[d]) {
+            b = (c * P.cal_nt[d] - sn * st) / det;
+            a = (st - b * sn) / c;
+            if (a < 0 || b <= 0) {                                      // keep the model physical
+                a = 0.0;
+                b = st / sn;
+            }
+        }
+        per[d] = b;
+        fixed += a;
+    }
+    m->offload_ms_per_block = per[0];
+    m->upload_ms_per_block = per[1];
+    m->fixed_ms = fixed;
     return TC_OK;
 }
 

@@ -398,3 +398,39 @@ def test_calibrate_keeps_pool_and_sets_auto():
     o.sync()
     compare_full(o, c, "after calibrate")
     c.close()
+
+
+def test_xfer_model_calibrates_from_measured_transfers():
+    """NEXT-3's T_transfer comes from this pool's own measured transfers (tc_xfer_model_measure): after offloads and
+    uploads of 1..64 blocks the fitted line has a per-block cost between a 10 and a 100 GB/s link and a small
+    non-negative fixed cost, and it predicts a 64-block round trip within 35 % of the measured one."""
+    import time
+    from paper_2510_18586_b200 import sched
+    L, H, D, N, S = 28, 4, 128, 512, 256                    # C2-shaped 896 KiB blocks
+    c = tcb.Pool(L, H, D, 16, "bf16", N, device=0, host_slots=S, n_classes=2, xfer_d2h=tcb.XFER_STAGED,
+                 xfer_h2d=tcb.XFER_STAGED)
+    c.fill(5)
+    c.timing(1)
+    c.agent_add(0, 0)
+    c.alloc(0, 64)
+    for n in (1, 4, 16, 64, 1, 4, 16, 64):
+        h = c.offload(0, c.block_table(0)[:n])
+        c.sync()
+        c.upload(h)
+        c.sync()
+    m = sched.xfer_model_measure(c)
+    B = c.block_bytes
+    for k in ("offload_ms_per_block", "upload_ms_per_block"):
+        assert B / 100e9 * 1e3 < m[k] < B / 10e9 * 1e3, m
+    assert 0.0 <= m["fixed_ms"] < 0.5, m
+    t0 = time.perf_counter()
+    h = c.offload(0, c.block_table(0))
+    c.wait(h)
+    c.sync()
+    c.upload(h)
+    c.wait(h)
+    wall_ms = (time.perf_counter() - t0) * 1e3
+    c.sync()
+    pred = sched.transfer_ms(64, m["offload_ms_per_block"], m["upload_ms_per_block"], m["fixed_ms"])
+    assert 0.65 * wall_ms < pred < 1.35 * wall_ms, (pred, wall_ms, m)
+    c.close()
