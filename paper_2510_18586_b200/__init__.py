@@ -231,6 +231,12 @@ class Pool:
             import torch   # hand the pool's HBM back (the caching allocator would keep tens of GiB reserved)
             torch.cuda.empty_cache()
 
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
     def __del__(self):
         try:
             self.close()
