@@ -305,6 +305,50 @@ typedef struct tc_upload_plan { int32_t immediate; double upload_start, reservat
 tc_status tc_plan_upload(double call_start, double t_final, double upload_ms, double offload_ms, double lead_ms,
                          tc_upload_plan *out);
 
+/* ---- NEXT-3: the Time Scheduler as a runtime (§4.1-4.3; SPEC time_scheduler S:214-304) ------------
+   An event machine over a pool, driven by the serving engine with its own clock (ms; reading C2):
+     tc_ts_call_start  a function call starts: Eq. 1 forecast over the (agent class, label) EWMA table, T_transfer
+                       from params.model, Alg. 1 against the caller's waiting queue; on "offload" the agent's on-GPU
+                       blocks are offloaded (tc_offload; NOHOST leaves it retained, reported in out->status) and the
+                       predictive upload is planned (tc_plan_upload, lead_ms).
+     tc_ts_tick        per agent in id order: begin the gradual reservation reserve_cycles ticks (tick_ms apart)
+                       before its deadline (tc_reserve_begin), one tc_reserve_tick, then issue the uploads whose start
+                       time has come (tc_upload; NOBLOCKS -> retried at the next tick).
+     tc_ts_call_finish the call returned: record the observation (EWMA), then *wait_handle = 0 (retained: resume now)
+                       or the upload's handle, uploading immediately if the planned upload was not issued yet (early
+                       return).  The engine must tc_wait / tc_stream_wait on that handle before decoding
+                       (S:283).  TC_E_NOBLOCKS: no device blocks for the upload yet; nothing else changed; retry.
+   Errors: TC_E_INVAL for an unknown agent, a call_start on an agent already in a call, a call_finish on one that is
+   not.  Single writer, like the pool. */
+typedef struct tc_ts tc_ts;
+typedef struct tc_ts_params {
+    double alpha, beta;          /* Eq. 1 hint weight, EWMA weight (0.5, 0.5; B10) */
+    double cold_start_ms;        /* forecast before any observation and without a hint (100) */
+    double lead_ms;              /* reservation ready this long before the upload starts (100) */
+    double tick_ms;              /* the engine's scheduling-tick period (10) */
+    int32_t reserve_cycles;      /* gradual reservation chunks, 0 = none (4) */
+    double v_tokens_per_s;       /* engine throughput for Alg. 1's N_capacity (1000) */
+    tc_xfer_model model;         /* T_transfer (default: SPEC's 60 ms round trip per 4096 blocks; better: the
+                                    pool's own tc_xfer_model_measure) */
+} tc_ts_params;
+void tc_ts_params_init(tc_ts_params *prm);
+tc_status tc_ts_create(tc_pool *p, const tc_ts_params *prm, tc_ts **out);
+void tc_ts_destroy(tc_ts *s);
+typedef struct tc_ts_decision {
+    int32_t offload;             /* 1 = the agent's blocks were offloaded */
+    int32_t match;               /* Alg. 1's best-fit waiting request, -1 = none */
+    int32_t status;              /* TC_OK, or TC_E_NOHOST when Alg. 1 said offload but the host buffer refused */
+    double t_fc, t_transfer;     /* forecast and T_transfer (ms) */
+    double upload_start, reservation_start;   /* plan (engine clock, ms); 0 when retained */
+    tc_handle handle;            /* the offload's handle, 0 when retained */
+} tc_ts_decision;
+tc_status tc_ts_call_start(tc_ts *s, int32_t agent, int32_t label, double now_ms, double t_req_ms,
+                           const double *waiting_tokens, int64_t n_waiting, tc_ts_decision *out);
+tc_status tc_ts_tick(tc_ts *s, double now_ms, int32_t *uploads_issued);
+tc_status tc_ts_call_finish(tc_ts *s, int32_t agent, double now_ms, tc_handle *wait_handle);
+/* The forecast table entry of (agent class, label): t_hist and n_obs (0 / 0 before any observation). */
+tc_status tc_ts_forecast(tc_ts *s, int32_t agent_class, int32_t label, double *t_hist, int64_t *n_obs);
+
 /* ---- NEXT-4: Space-Scheduler partitions (§5), host-only ------------------------------------------ */
 double tc_static_priority(double w_static, int32_t node_depth, int32_t node_out_degree);
 /* time_wait * ln(max(tokens_req / max(time_wait, 1 ms), 1)) (clamp: DESIGN.md B7) */

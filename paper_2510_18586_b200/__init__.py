@@ -35,7 +35,8 @@ SYMBOLS = [
     # decision layers (paper_2510_18586_b200/sched.py binds them)
     "tc_fc_predict", "tc_fc_observe", "tc_transfer_ms", "tc_xfer_model_measure", "tc_should_offload",
     "tc_plan_upload", "tc_static_priority", "tc_dynamic_priority", "tc_select_critical", "tc_update_reservations",
-    "tc_apply_reservations",
+    "tc_apply_reservations", "tc_ts_params_init", "tc_ts_create", "tc_ts_destroy", "tc_ts_call_start", "tc_ts_tick",
+    "tc_ts_call_finish", "tc_ts_forecast",
 ]
 
 

@@ -7,7 +7,9 @@
 // Readings where the paper is silent are DESIGN.md B6-B9 (SPEC.md's choices); the CPU oracle is oracle/scheduler.py.
 #include <algorithm>
 #include <cmath>
+#include <map>
 #include <numeric>
+#include <utility>
 #include <vector>
 
 #include "runtime.hpp"
@@ -163,6 +165,193 @@ tc_status tc_apply_reservations(tc_pool *p, int32_t n, const int32_t *classes, c
     for (int64_t r : next) sum += r;
     if (sum > P.N) return TC_E_INVAL;
     P.alloc.reserved = next;                                             // lazy shrink: claimed untouched
+    return TC_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------------------------ NEXT-3 runtime
+// The Time Scheduler as an event machine (include/tokencake.h "NEXT-3: the Time Scheduler as a runtime"; DESIGN.md
+// reading C2; oracle: oracle/time_scheduler.py).
+struct tc_ts {
+    tc_pool *pool = nullptr;
+    tc_ts_params prm{};
+    std::map<std::pair<int32_t, int32_t>, tc_fc_stat> table;   // (agent class, label) -> EWMA state
+    struct Call {
+        int32_t label = 0, cls = 0;
+        double start = 0, upload_start = 0, resv_start = 0;
+        bool off = false, up = false, resv = false, finished = false;
+        tc_handle h = 0;
+    };
+    std::map<int32_t, Call> calls;                               // agents in a call, by id
+    std::vector<int32_t> ids, new_ids;                           // scratch
+};
+
+extern "C" {
+
+void tc_ts_params_init(tc_ts_params *prm) {
+    if (!prm) return;
+    *prm = tc_ts_params{0.5, 0.5, 100.0, 100.0, 10.0, 4, 1000.0, {30.0 / 4096, 30.0 / 4096, 0.0}};
+}
+
+tc_status tc_ts_create(tc_pool *p, const tc_ts_params *prm, tc_ts **out) {
+    if (!p || !out) return TC_E_INVAL;
+    tc_ts_params d;
+    tc_ts_params_init(&d);
+    if (prm) d = *prm;
+    if (d.reserve_cycles < 0 || d.tick_ms < 0 || d.v_tokens_per_s < 0 || d.alpha < 0 || d.alpha > 1 ||
+        d.beta < 0 || d.beta > 1)
+        return TC_E_INVAL;
+    try {
+        tc_ts *s = new tc_ts();
+        s->pool = p;
+        s->prm = d;
+        *out = s;
+    } catch (...) {
+        return TC_E_OOM;
+    }
+    return TC_OK;
+}
+
+void tc_ts_destroy(tc_ts *s) { delete s; }
+
+tc_status tc_ts_call_start(tc_ts *s, int32_t agent, int32_t label, double now_ms, double t_req_ms,
+                           const double *waiting_tokens, int64_t n_waiting, tc_ts_decision *out) {
+    if (!s || !out || n_waiting < 0 || (n_waiting > 0 && !waiting_tokens)) return TC_E_INVAL;
+    try {
+        tc::Pool &P = s->pool->impl;
+        if (agent < 0 || agent >= P.max_agents || !P.agents[agent].exists || s->calls.count(agent)) return TC_E_INVAL;
+        const tc_ts_params &q = s->prm;
+        s->ids.clear();
+        for (int32_t b : P.agents[agent].table)
+            if (b >= 0) s->ids.push_back(b);
+        const int64_t n = (int64_t)s->ids.size();
+        tc_ts::Call c;
+        c.label = label;
+        c.cls = P.agents[agent].cls;
+        c.start = now_ms;
+        tc_fc_stat st{0.0, 0, q.cold_start_ms};
+        auto it = s->table.find({c.cls, label});
+        if (it != s->table.end()) st = it->second;
+        st.cold_start = q.cold_start_ms;
+        *out = tc_ts_decision{0, -1, TC_OK, tc_fc_predict(&st, t_req_ms, q.alpha), 0.0, 0.0, 0.0, 0};   // Eq. 1
+        out->t_transfer = tc_transfer_ms(&q.model, n);
+        if (n > 0) {
+            tc_offload_decision d;
+            tc_status r = tc_should_offload(n, out->t_fc, out->t_transfer, q.v_tokens_per_s, waiting_tokens,
+                                            n_waiting, &d);                                              // Alg. 1
+            if (r != TC_OK) return r;
+            out->match = d.match;
+            if (d.offload) {
+                tc_handle h = 0;
+                const int64_t off[2] = {0, n};
+                r = P.offload_batch(1, &agent, off, s->ids.data(), &h);
+                if (r == TC_E_NOHOST) {
+                    out->status = TC_E_NOHOST;                 // refused: the request keeps its blocks
+                } else if (r != TC_OK) {
+                    return r;
+                } else {
+                    tc_upload_plan plan;
+                    tc_plan_upload(now_ms, out->t_fc, (double)n * q.model.upload_ms_per_block,
+                                   (double)n * q.model.offload_ms_per_block, q.lead_ms, &plan);
+                    c.off = true;
+                    c.h = h;
+                    c.upload_start = plan.upload_start;
+                    c.resv_start = plan.reservation_deadline - q.reserve_cycles * q.tick_ms;
+                    out->offload = 1;
+                    out->handle = h;
+                    out->upload_start = c.upload_start;
+                    out->reservation_start = c.resv_start;
+                }
+            }
+        }
+        s->calls[agent] = c;
+        if (P.check) P.check_invariants("tc_ts_call_start");
+        return TC_OK;
+    } catch (...) {
+        return TC_E_OOM;
+    }
+}
+
+tc_status tc_ts_tick(tc_ts *s, double now_ms, int32_t *uploads_issued) {
+    if (!s) return TC_E_INVAL;
+    try {
+        tc::Pool &P = s->pool->impl;
+        int32_t issued = 0;
+        for (auto &kv : s->calls) {                        // gradual reservation, ready by its deadline
+            tc_ts::Call &c = kv.second;
+            if (c.off && !c.up && !c.finished && !c.resv && s->prm.reserve_cycles > 0 && now_ms >= c.resv_start) {
+                const tc_status r = P.reserve_begin(c.h, s->prm.reserve_cycles);
+                if (r != TC_OK) return r;
+                c.resv = true;
+            }
+        }
+        tc_status r = P.reserve_tick();
+        if (r != TC_OK) return r;
+        for (auto &kv : s->calls) {                        // predictive uploads that are due
+            tc_ts::Call &c = kv.second;
+            if (!c.off || c.up || c.finished || now_ms < c.upload_start) continue;
+            auto hit = P.handles.find(c.h);
+            if (hit == P.handles.end()) return TC_E_HANDLE;
+            s->new_ids.resize(hit->second.pos.size());
+            const int64_t off[2] = {0, (int64_t)hit->second.pos.size()};
+            r = P.upload_batch(1, &c.h, off, s->new_ids.data());
+            if (r == TC_E_NOBLOCKS) continue;              // "stalls": retried next tick
+            if (r != TC_OK) return r;
+            c.up = true;
+            ++issued;
+        }
+        if (uploads_issued) *uploads_issued = issued;
+        if (P.check) P.check_invariants("tc_ts_tick");
+        return TC_OK;
+    } catch (...) {
+        return TC_E_OOM;
+    }
+}
+
+tc_status tc_ts_call_finish(tc_ts *s, int32_t agent, double now_ms, tc_handle *wait_handle) {
+    if (!s || !wait_handle) return TC_E_INVAL;
+    try {
+        auto it = s->calls.find(agent);
+        if (it == s->calls.end()) return TC_E_INVAL;
+        tc_ts::Call &c = it->second;
+        if (!c.finished) {                                 // EWMA feedback
+            if (now_ms - c.start > 0) {
+                tc_fc_stat &st = s->table.emplace(std::make_pair(c.cls, c.label),
+                                                  tc_fc_stat{0.0, 0, s->prm.cold_start_ms}).first->second;
+                tc_fc_observe(&st, now_ms - c.start, s->prm.beta);
+            }
+            c.finished = true;
+        }
+        if (!c.off) {
+            *wait_handle = 0;                              // retained: resume at once
+            s->calls.erase(it);
+            return TC_OK;
+        }
+        if (!c.up) {                                       // early return: immediate upload
+            tc::Pool &P = s->pool->impl;
+            auto hit = P.handles.find(c.h);
+            if (hit == P.handles.end()) return TC_E_HANDLE;
+            s->new_ids.resize(hit->second.pos.size());
+            const int64_t off[2] = {0, (int64_t)hit->second.pos.size()};
+            const tc_status r = P.upload_batch(1, &c.h, off, s->new_ids.data());
+            if (r != TC_OK) return r;                      // NOBLOCKS: nothing else changed; retry
+            c.up = true;
+        }
+        *wait_handle = c.h;
+        s->calls.erase(it);
+        if (s->pool->impl.check) s->pool->impl.check_invariants("tc_ts_call_finish");
+        return TC_OK;
+    } catch (...) {
+        return TC_E_OOM;
+    }
+}
+
+tc_status tc_ts_forecast(tc_ts *s, int32_t agent_class, int32_t label, double *t_hist, int64_t *n_obs) {
+    if (!s || !t_hist || !n_obs) return TC_E_INVAL;
+    auto it = s->table.find({agent_class, label});
+    *t_hist = it == s->table.end() ? 0.0 : it->second.t_hist;
+    *n_obs = it == s->table.end() ? 0 : it->second.n_obs;
     return TC_OK;
 }
 

@@ -51,6 +51,27 @@ _SIG = {
                                      ctypes.POINTER(D), ctypes.POINTER(I64)]),
     "tc_apply_reservations": (I32, [P, I32, ctypes.POINTER(I32), ctypes.POINTER(I64)]),
 }
+
+
+class TsParams(ctypes.Structure):
+    _fields_ = [("alpha", D), ("beta", D), ("cold_start_ms", D), ("lead_ms", D), ("tick_ms", D),
+                ("reserve_cycles", I32), ("v_tokens_per_s", D), ("model", XferModel)]
+
+
+class TsDecision(ctypes.Structure):
+    _fields_ = [("offload", I32), ("match", I32), ("status", I32), ("t_fc", D), ("t_transfer", D),
+                ("upload_start", D), ("reservation_start", D), ("handle", ctypes.c_uint64)]
+
+
+_SIG.update({
+    "tc_ts_params_init": (None, [ctypes.POINTER(TsParams)]),
+    "tc_ts_create": (I32, [P, ctypes.POINTER(TsParams), ctypes.POINTER(P)]),
+    "tc_ts_destroy": (None, [P]),
+    "tc_ts_call_start": (I32, [P, I32, I32, D, D, ctypes.POINTER(D), I64, ctypes.POINTER(TsDecision)]),
+    "tc_ts_tick": (I32, [P, D, ctypes.POINTER(I32)]),
+    "tc_ts_call_finish": (I32, [P, I32, D, ctypes.POINTER(ctypes.c_uint64)]),
+    "tc_ts_forecast": (I32, [P, I32, I32, ctypes.POINTER(D), ctypes.POINTER(I64)]),
+})
 for _n, (_r, _a) in _SIG.items():
     _f = getattr(lib, _n)
     _f.restype, _f.argtypes = _r, _a
@@ -99,6 +120,60 @@ def plan_upload(call_start, t_final, upload_ms, offload_ms, lead_ms=100.0) -> di
     _check(lib.tc_plan_upload(call_start, t_final, upload_ms, offload_ms, lead_ms, ctypes.byref(out)))
     return {"immediate": bool(out.immediate), "upload_start": out.upload_start,
             "reservation_deadline": out.reservation_deadline, "predicted_finish": out.predicted_finish}
+
+
+# ------------------------------------------------------------------------------------------------ NEXT-3 runtime
+class TimeScheduler:
+    """The Time Scheduler as an event machine over a Pool (tc_ts_*): call_start / tick / call_finish with the
+    engine's clock in ms.  Keyword parameters as tc_ts_params (model = dict of xfer_model_measure's keys)."""
+
+    def __init__(self, pool, **kw):
+        prm = TsParams()
+        lib.tc_ts_params_init(ctypes.byref(prm))
+        model = kw.pop("model", None)
+        for k, v in kw.items():
+            setattr(prm, k, v)
+        if model is not None:
+            prm.model = XferModel(model["offload_ms_per_block"], model["upload_ms_per_block"],
+                                  model.get("fixed_ms", 0.0))
+        h = ctypes.c_void_p()
+        _check(lib.tc_ts_create(pool._h, ctypes.byref(prm), ctypes.byref(h)))
+        self._h, self.pool = h, pool
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.tc_ts_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def call_start(self, agent: int, label: int, now: float, t_req=None, waiting=()) -> dict:
+        w = np.ascontiguousarray(np.asarray(list(waiting), dtype=np.float64).reshape(-1))
+        out = TsDecision()
+        _check(lib.tc_ts_call_start(self._h, agent, label, now, -1.0 if t_req is None else float(t_req),
+                                    _ptr(w, D) if w.size else None, w.size, ctypes.byref(out)))
+        return {"offload": bool(out.offload), "match": out.match, "status": out.status, "t_fc": out.t_fc,
+                "t_transfer": out.t_transfer, "upload_start": out.upload_start,
+                "reservation_start": out.reservation_start, "handle": out.handle}
+
+    def tick(self, now: float) -> int:
+        n = ctypes.c_int32()
+        _check(lib.tc_ts_tick(self._h, now, ctypes.byref(n)))
+        return n.value
+
+    def call_finish(self, agent: int, now: float) -> int:
+        h = ctypes.c_uint64()
+        _check(lib.tc_ts_call_finish(self._h, agent, now, ctypes.byref(h)))
+        return h.value
+
+    def forecast(self, agent_class: int, label: int) -> tuple:
+        t, n = ctypes.c_double(), ctypes.c_int64()
+        _check(lib.tc_ts_forecast(self._h, agent_class, label, ctypes.byref(t), ctypes.byref(n)))
+        return (t.value if n.value else None), n.value
 
 
 # ------------------------------------------------------------------------------------------------ NEXT-4

@@ -434,3 +434,47 @@ def test_xfer_model_calibrates_from_measured_transfers():
     pred = sched.transfer_ms(64, m["offload_ms_per_block"], m["upload_ms_per_block"], m["fixed_ms"])
     assert 0.65 * wall_ms < pred < 1.35 * wall_ms, (pred, wall_ms, m)
     c.close()
+
+
+def test_time_scheduler_runtime_bytes():
+    """The native Time Scheduler (tc_ts_*) driving a device pool through a random event stream, against the oracle
+    event machine on a byte-level pool: identical decisions and handles, and after the stream the KV bytes, tables
+    and counters match exactly."""
+    from oracle.time_scheduler import TimeSchedulerOracle
+    from paper_2510_18586_b200 import sched
+    L, H, D, N, S = 2, 2, 64, 160, 48
+    rng = np.random.default_rng(4)
+    pool0 = content.pool_bytes(6, L, N, 16, H, D)
+    o = OraclePool(N, S, n_classes=2, store=BytesStore(pool0, S))
+    c = dev_pool(L, H, D, N, S, "staged", ncls=2, seed=6)
+    for a in range(5):
+        n = int(rng.integers(2, 20))
+        o.agent_add(a, a % 2)
+        c.agent_add(a, a % 2)
+        assert o.alloc(a, n) == list(c.alloc(a, n))
+    prm = dict(v_tokens_per_s=4000.0, tick_ms=5.0, reserve_cycles=2, lead_ms=10.0, cold_start_ms=60.0)
+    model = {"offload_ms_per_block": 0.1, "upload_ms_per_block": 0.1, "fixed_ms": 0.0}
+    to = TimeSchedulerOracle(o, offload_ms_per_block=0.1, upload_ms_per_block=0.1, **prm)
+    tc = sched.TimeScheduler(c, model=model, **prm)
+    now = 0.0
+    for _ in range(300):
+        now += float(rng.integers(1, 12))
+        a = int(rng.integers(0, 5))
+        if a in to.stalled():
+            if rng.random() < 0.4:
+                assert to.call_finish(a, now) == tc.call_finish(a, now)
+        else:
+            w = [float(x) for x in rng.integers(1, 300, size=2)]
+            x, y = to.call_start(a, 0, now, waiting=w), tc.call_start(a, 0, now, waiting=w)
+            assert (x["offload"], x["handle"]) == (y["offload"], y["handle"])
+        assert to.tick(now) == tc.tick(now)
+        if rng.random() < 0.2:
+            o.sync()
+            c.sync()
+    for a in list(to.stalled()):
+        assert to.call_finish(a, now + 1000.0) == tc.call_finish(a, now + 1000.0)
+    o.sync()
+    c.sync()
+    compare_full(o, c, "after the time-scheduler stream")
+    tc.close()
+    c.close()
