@@ -367,6 +367,29 @@ tc_status tc_update_reservations(const tc_partition_params *pp, double *total_re
 /* Apply quotas to the pool's classes at once (tc_partition_reserve semantics, all-or-nothing, lazy shrink). */
 tc_status tc_apply_reservations(tc_pool *p, int32_t n, const int32_t *classes, const int64_t *reserve_num);
 
+/* ---- NEXT-4 as a runtime: one Space-Scheduler partition update over a pool (SPEC space_scheduler; reading C3) --
+   Agent types are the pool's classes.  tc_ss_update: combined score[c] = static_score[c] + sum of
+   tc_dynamic_priority over the waiting requests of class c; the top critical_ratio classes are critical
+   (tc_select_critical); Alg. 2 (tc_update_reservations) runs on the pool's own usage (non-free blocks; per class the
+   on-GPU blocks of its agents) with the persistent total_reserve_ratio; the resulting quotas replace every class's
+   reservation at once (non-critical -> 0; lazy shrink).  Outputs (optional, n_classes entries): reserve_num,
+   critical flags, combined scores; *total_reserve_ratio = the ratio after Phase 1.  TC_E_INVAL on a waiting class
+   out of range.  tc_ss_critical_inversion: 1 iff the evicted class's last combined score is strictly higher than
+   the cause's ("critical inversion"). */
+typedef struct tc_ss tc_ss;
+typedef struct tc_ss_params {
+    tc_partition_params partition;   /* 0.85, 0.50, 0.05, 0.40 */
+    double critical_ratio;           /* 0.25 */
+    double initial_reserve_ratio;    /* 0 */
+} tc_ss_params;
+void tc_ss_params_init(tc_ss_params *prm);
+tc_status tc_ss_create(tc_pool *p, const tc_ss_params *prm, tc_ss **out);
+void tc_ss_destroy(tc_ss *s);
+tc_status tc_ss_update(tc_ss *s, const double *static_score, int64_t n_waiting, const int32_t *waiting_class,
+                       const double *time_wait_ms, const double *tokens_req, int64_t *reserve_num,
+                       uint8_t *critical, double *scores, double *total_reserve_ratio);
+tc_status tc_ss_critical_inversion(tc_ss *s, int32_t evicted_class, int32_t cause_class, int32_t *inversion);
+
 /* ---- device tier (staged halves; NEXT-2 building block) ---------------------------------------------------- */
 /* Gather blocks ids[0..n) into a contiguous device buffer dst[n][L][2][C] (the HBM-bound KG1 kernel), or scatter
    src[n][L][2][C] into blocks ids[0..n) (KS1), on `cuda_stream` (NULL = the offload stream).  No allocator or

@@ -36,7 +36,8 @@ SYMBOLS = [
     "tc_fc_predict", "tc_fc_observe", "tc_transfer_ms", "tc_xfer_model_measure", "tc_should_offload",
     "tc_plan_upload", "tc_static_priority", "tc_dynamic_priority", "tc_select_critical", "tc_update_reservations",
     "tc_apply_reservations", "tc_ts_params_init", "tc_ts_create", "tc_ts_destroy", "tc_ts_call_start", "tc_ts_tick",
-    "tc_ts_call_finish", "tc_ts_forecast",
+    "tc_ts_call_finish", "tc_ts_forecast", "tc_ss_params_init", "tc_ss_create", "tc_ss_destroy", "tc_ss_update",
+    "tc_ss_critical_inversion",
 ]
 
 

@@ -356,3 +356,96 @@ tc_status tc_ts_forecast(tc_ts *s, int32_t agent_class, int32_t label, double *t
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------------------------------------ NEXT-4 runtime
+// One Space-Scheduler partition update over a pool (include/tokencake.h; reading C3; oracle:
+// oracle/space_scheduler.py).
+struct tc_ss {
+    tc_pool *pool = nullptr;
+    tc_ss_params prm{};
+    double ratio = 0.0;
+    std::vector<double> scores;
+};
+
+extern "C" {
+
+void tc_ss_params_init(tc_ss_params *prm) {
+    if (!prm) return;
+    *prm = tc_ss_params{{0.85, 0.50, 0.05, 0.40}, 0.25, 0.0};
+}
+
+tc_status tc_ss_create(tc_pool *p, const tc_ss_params *prm, tc_ss **out) {
+    if (!p || !out) return TC_E_INVAL;
+    tc_ss_params d;
+    tc_ss_params_init(&d);
+    if (prm) d = *prm;
+    if (!(d.critical_ratio > 0 && d.critical_ratio <= 1) || d.initial_reserve_ratio < 0) return TC_E_INVAL;
+    try {
+        tc_ss *s = new tc_ss();
+        s->pool = p;
+        s->prm = d;
+        s->ratio = d.initial_reserve_ratio;
+        *out = s;
+    } catch (...) {
+        return TC_E_OOM;
+    }
+    return TC_OK;
+}
+
+void tc_ss_destroy(tc_ss *s) { delete s; }
+
+tc_status tc_ss_update(tc_ss *s, const double *static_score, int64_t n_waiting, const int32_t *waiting_class,
+                       const double *time_wait_ms, const double *tokens_req, int64_t *reserve_num,
+                       uint8_t *critical, double *scores, double *total_reserve_ratio) {
+    if (!s || !static_score || n_waiting < 0 ||
+        (n_waiting > 0 && (!waiting_class || !time_wait_ms || !tokens_req)))
+        return TC_E_INVAL;
+    try {
+        tc::Pool &P = s->pool->impl;
+        const int32_t n = P.n_classes;
+        std::vector<double> sc(static_score, static_score + n);
+        for (int64_t i = 0; i < n_waiting; ++i) {          // hybrid score: static + sum of dynamic
+            if (waiting_class[i] < 0 || waiting_class[i] >= n) return TC_E_INVAL;
+            sc[waiting_class[i]] += tc_dynamic_priority(time_wait_ms[i], tokens_req[i]);
+        }
+        std::vector<uint8_t> crit(n, 0);
+        tc_status r = tc_select_critical(n, sc.data(), s->prm.critical_ratio, crit.data());
+        if (r != TC_OK) return r;
+        std::vector<int64_t> per(n, 0);                    // the pool's own usage, per class
+        for (int32_t a = 0; a < P.max_agents; ++a) {
+            const tc::AgentRec &ag = P.agents[a];
+            if (!ag.exists) continue;
+            for (int32_t b : ag.table)
+                if (b >= 0 && P.alloc.state[b] == tc::kAlloc) ++per[ag.cls];
+        }
+        const int64_t usage = P.N - P.alloc.nfree;
+        double ratio = s->ratio, r_total = 0.0;
+        std::vector<int64_t> res(n, 0);
+        r = tc_update_reservations(&s->prm.partition, &ratio, usage, P.N, n, crit.data(), sc.data(), per.data(),
+                                   &r_total, res.data());                                       // Alg. 2
+        if (r != TC_OK) return r;
+        std::vector<int32_t> cls(n);
+        std::iota(cls.begin(), cls.end(), 0);
+        if ((r = tc_apply_reservations(s->pool, n, cls.data(), res.data())) != TC_OK) return r;
+        s->ratio = ratio;
+        s->scores = sc;
+        if (reserve_num) std::copy(res.begin(), res.end(), reserve_num);
+        if (critical) std::copy(crit.begin(), crit.end(), critical);
+        if (scores) std::copy(sc.begin(), sc.end(), scores);
+        if (total_reserve_ratio) *total_reserve_ratio = ratio;
+        if (P.check) P.check_invariants("tc_ss_update");
+        return TC_OK;
+    } catch (...) {
+        return TC_E_OOM;
+    }
+}
+
+tc_status tc_ss_critical_inversion(tc_ss *s, int32_t evicted_class, int32_t cause_class, int32_t *inversion) {
+    if (!s || !inversion) return TC_E_INVAL;
+    const int32_t n = (int32_t)s->scores.size();
+    auto score = [&](int32_t c) { return c >= 0 && c < n ? s->scores[c] : 0.0; };
+    *inversion = score(evicted_class) > score(cause_class) ? 1 : 0;
+    return TC_OK;
+}
+
+}  // extern "C"

@@ -63,7 +63,18 @@ class TsDecision(ctypes.Structure):
                 ("upload_start", D), ("reservation_start", D), ("handle", ctypes.c_uint64)]
 
 
+class SsParams(ctypes.Structure):
+    _fields_ = [("partition", PartitionParams), ("critical_ratio", D), ("initial_reserve_ratio", D)]
+
+
 _SIG.update({
+    "tc_ss_params_init": (None, [ctypes.POINTER(SsParams)]),
+    "tc_ss_create": (I32, [P, ctypes.POINTER(SsParams), ctypes.POINTER(P)]),
+    "tc_ss_destroy": (None, [P]),
+    "tc_ss_update": (I32, [P, ctypes.POINTER(D), I64, ctypes.POINTER(I32), ctypes.POINTER(D), ctypes.POINTER(D),
+                           ctypes.POINTER(I64), ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(D),
+                           ctypes.POINTER(D)]),
+    "tc_ss_critical_inversion": (I32, [P, I32, I32, ctypes.POINTER(I32)]),
     "tc_ts_params_init": (None, [ctypes.POINTER(TsParams)]),
     "tc_ts_create": (I32, [P, ctypes.POINTER(TsParams), ctypes.POINTER(P)]),
     "tc_ts_destroy": (None, [P]),
@@ -216,3 +227,52 @@ def apply_reservations(pool, quotas: dict):
     cls = np.asarray(list(quotas.keys()), dtype=np.int32)
     num = np.asarray(list(quotas.values()), dtype=np.int64)
     _check(lib.tc_apply_reservations(pool._h, len(cls), _ptr(cls, I32), _ptr(num, I64)))
+
+
+# ------------------------------------------------------------------------------------------------ NEXT-4 runtime
+class SpaceScheduler:
+    """One Space-Scheduler partition update per call over a Pool (tc_ss_*): the pool's classes are the agent types,
+    Alg. 2 reads the pool's own usage, the quotas are applied to the pool."""
+
+    def __init__(self, pool, critical_ratio=0.25, initial_reserve_ratio=0.0, gpu_usage_high=0.85,
+                 gpu_usage_low=0.50, adjustment_step=0.05, reserve_ratio_max=0.40):
+        prm = SsParams(PartitionParams(gpu_usage_high, gpu_usage_low, adjustment_step, reserve_ratio_max),
+                       critical_ratio, initial_reserve_ratio)
+        h = ctypes.c_void_p()
+        _check(lib.tc_ss_create(pool._h, ctypes.byref(prm), ctypes.byref(h)))
+        self._h, self.pool, self.n = h, pool, pool.stats()["n_classes"]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.tc_ss_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def update(self, static_scores, waiting=()) -> dict:
+        """static_scores: one per class; waiting: [(class, time_wait_ms, tokens_req), ...]."""
+        st = np.ascontiguousarray(np.asarray(static_scores, dtype=np.float64).reshape(-1))
+        if st.size != self.n:
+            raise TcError(-1, "one static score per class")
+        w = list(waiting)
+        wc = np.ascontiguousarray(np.asarray([x[0] for x in w], dtype=np.int32))
+        wt = np.ascontiguousarray(np.asarray([x[1] for x in w], dtype=np.float64))
+        wk = np.ascontiguousarray(np.asarray([x[2] for x in w], dtype=np.float64))
+        res = np.zeros(self.n, dtype=np.int64)
+        crit = np.zeros(self.n, dtype=np.uint8)
+        sc = np.zeros(self.n, dtype=np.float64)
+        ratio = ctypes.c_double()
+        _check(lib.tc_ss_update(self._h, _ptr(st, D), len(w), _ptr(wc, I32) if w else None,
+                                _ptr(wt, D) if w else None, _ptr(wk, D) if w else None, _ptr(res, I64),
+                                _ptr(crit, ctypes.c_uint8), _ptr(sc, D), ctypes.byref(ratio)))
+        return {"reserve": [int(x) for x in res], "critical": [bool(x) for x in crit], "ratio": ratio.value,
+                "scores": [float(x) for x in sc]}
+
+    def critical_inversion(self, evicted_cls: int, cause_cls: int) -> bool:
+        r = ctypes.c_int32()
+        _check(lib.tc_ss_critical_inversion(self._h, evicted_cls, cause_cls, ctypes.byref(r)))
+        return bool(r.value)
