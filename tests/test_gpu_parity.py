@@ -27,7 +27,8 @@ MODES = {"direct": (tcb.XFER_DIRECT, tcb.XFER_DIRECT, 0), "staged": (tcb.XFER_ST
          "staged_tma": (tcb.XFER_STAGED, tcb.XFER_STAGED, 1), "direct_tile": (tcb.XFER_DIRECT, tcb.XFER_DIRECT, 2),
          "staged_tile": (tcb.XFER_STAGED, tcb.XFER_STAGED, 2), "staged_tma4": (tcb.XFER_STAGED, tcb.XFER_STAGED, 3),
          "mixed_rev": (tcb.XFER_STAGED, tcb.XFER_DIRECT, 2), "copy": (tcb.XFER_COPY, tcb.XFER_COPY, 0),
-         "copy_staged": (tcb.XFER_COPY, tcb.XFER_STAGED, 3), "staged_copy": (tcb.XFER_STAGED, tcb.XFER_COPY, 3)}
+         "copy_staged": (tcb.XFER_COPY, tcb.XFER_STAGED, 3), "staged_copy": (tcb.XFER_STAGED, tcb.XFER_COPY, 3),
+         "auto": (tcb.XFER_AUTO, tcb.XFER_AUTO, 3)}
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -478,3 +479,14 @@ def test_time_scheduler_runtime_bytes():
     compare_full(o, c, "after the time-scheduler stream")
     tc.close()
     c.close()
+
+
+@pytest.mark.parametrize("mode,P", [("auto", 0), ("staged_tile", 0), ("direct", 0), ("staged", 6)])
+def test_long_random_stream_with_invariant_checks(monkeypatch, mode, P):
+    """Stress: 8,000 random ops (gradual reservation on, uploads issued before their offloads finished, ring reuse
+    through a 3-block staging buffer) on one pool with TC_CHECK=1 (SPEC invariants re-derived after every call);
+    the whole pool, every table and every counter equal the oracle's at every sync."""
+    monkeypatch.setenv("TC_CHECK", "1")
+    L, H, D, N, S, T = 3, 2, 64, 50, 20, 16
+    ops = fuzz_script(4242 + P, n_ops=8000, n_agents=4, n_classes=2, N=N, max_alloc=6, gradual=True)
+    run_script(ops, L, H, D, N, S, mode, ncls=2, seed=9, staging=3 * 2 * L * T * H * D * 2, T=T, P=P)
