@@ -506,12 +506,16 @@ tc_status Pool::calibrate(int64_t probe_bytes, tc_calibration_t *out) {
                 st = cuda_fail(cudaGetLastError(), "calibrate sync");
                 break;
             }
-            cudaEventRecord(e0, s_off);
-            cudaStreamWaitEvent(s_up, e0, 0);
+            if (cudaEventRecord(e0, s_off) != cudaSuccess || cudaStreamWaitEvent(s_up, e0, 0) != cudaSuccess) {
+                st = cuda_fail(cudaGetLastError(), "calibrate event");
+                break;
+            }
             if ((st = enqueue_xfer(true, modes[c >> 1], da, sa, s_off)) != TC_OK) break;
             if ((st = enqueue_xfer(false, modes[c & 1], db, sb, s_up)) != TC_OK) break;
-            cudaEventRecord(e1, s_off);
-            cudaEventRecord(e2, s_up);
+            if (cudaEventRecord(e1, s_off) != cudaSuccess || cudaEventRecord(e2, s_up) != cudaSuccess) {
+                st = cuda_fail(cudaGetLastError(), "calibrate event");
+                break;
+            }
             float t1 = 0.f, t2 = 0.f;
             if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventSynchronize(e2) != cudaSuccess ||
                 cudaEventElapsedTime(&t1, e0, e1) != cudaSuccess || cudaEventElapsedTime(&t2, e0, e2) != cudaSuccess) {
