@@ -233,9 +233,9 @@ def run_ours(args):
     gen = CycleGen(cfg, agents, combined=True)
     handles, sizes = {}, {}
 
-    def cycle(record=None):
-        """One scheduling cycle through the public API (tc_cycle: uploads then offloads, then tc_sync);
-        returns (blocks_up, blocks_off)."""
+    def cycle(record=None, retire=True):
+        """One scheduling cycle through the public API (tc_cycle: uploads then offloads, then tc_sync — skipped when
+        retire is False); returns (blocks_up, blocks_off)."""
         nu = no = 0
         for op in gen.next_cycle():
             if op[0] == "cycle":
@@ -259,7 +259,8 @@ def run_ours(args):
             elif op[0] == "sync":
                 if record is not None:
                     record("end")
-                pool.sync()
+                if retire:
+                    pool.sync()
         return nu, no
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
@@ -326,6 +327,7 @@ def run_ours(args):
                 f.write(json.dumps(r) + "\n")
     diag = pool.timing(0)
     tl_raw = pool.timeline(200000)
+    steady = steady_state(torch, dev, cycle, ups, offs_, B, min(args.steps, 40), pool, step_bytes, cfg.stall_cycles)
     tl_summary = timeline_summary(tl_raw)
     if os.environ.get("TC_DUMP_TIMELINE"):                 # debugging aid: raw per-span records of the diagnostic steps
         with open(os.environ["TC_DUMP_TIMELINE"], "w") as f:
@@ -442,6 +444,7 @@ def run_ours(args):
             "how": "sum of the transfer kernels' device durations / the steps' device time: the fraction of the step "
                    "during which this path occupies SMs (the copy-engine DMAs use none); rank 0"},
         "timeline": tl_summary,
+        "steady_state": steady,
         "hostlink_peak": link,
         "roofline": roof,
         "roofline_link": link_roof,
@@ -474,6 +477,39 @@ def ncu_traffic(cfg_name, kind, kd):
             "traffic_source": {"capture": os.path.relpath(path, ROOT), "dram_over_algorithmic": ratio,
                                "dram_read_over_algorithmic_read": statistics.mean(x["read_ratio"] for x in cap),
                                "note": "ncu counts writes still dirty in L2 at kernel end as not yet written"}}
+
+
+def steady_state(torch, dev, cycle, ups, offs, B, n, pool, step_bytes, stall_cycles):
+    """Diagnostic (not `value`): the same cycles enqueued back to back and retired (tc_sync) only every k cycles, as
+    a serving loop that does not drain the copy streams each cycle would run them — the host link then stays busy
+    across cycle boundaries.  k (<= 4) is the most cycles the pool's free blocks and host slots can carry without
+    retirement, judged from the timed steps' largest batches; k = 1 means no pipelining fits.  Device time from the
+    first cycle's start to the last one's end on both copy streams."""
+    s = pool.stats()
+    up_max = max(u for u, _ in step_bytes) // B
+    off_max = max(o for _, o in step_bytes) // B
+    k = 1
+    for kk in (4, 3, 2):
+        if s["free"] >= kk * up_max + off_max and s["host_free"] >= (kk + stall_cycles + 1) * off_max:
+            k = kk
+            break
+    torch.cuda.synchronize(dev)
+    e0 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e1 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    for e, s in zip(e0, (ups, offs)):
+        e.record(s)
+    moved = 0
+    for i in range(n):
+        last = i == n - 1
+        nu, no = cycle(retire=(i + 1) % k == 0 and not last)
+        moved += (nu + no) * B
+        if last:
+            for e, s in zip(e1, (ups, offs)):
+                e.record(s)
+    pool.sync()
+    ms = max(e0[a].elapsed_time(e1[b]) for a in range(2) for b in range(2))
+    return {"value": moved / (ms * 1e-3) / 1e9, "unit": "GB/s", "cycles": n, "sync_every": k,
+            "how": "cycles enqueued back to back, tc_sync every k cycles; bytes both directions / device time"}
 
 
 def timeline_summary(spans):
