@@ -237,6 +237,7 @@ def run_ours(args):
         """One scheduling cycle through the public API (tc_cycle: uploads then offloads, then tc_sync — skipped when
         retire is False); returns (blocks_up, blocks_off)."""
         nu = no = 0
+        started = False
         for op in gen.next_cycle():
             if op[0] == "cycle":
                 hs = np.array([handles.pop(a) for a in op[1]], dtype=np.uint64)
@@ -249,7 +250,8 @@ def run_ours(args):
                 ooff[1:] = np.cumsum([len(t) for t in tabs])
                 ids = np.ascontiguousarray(np.concatenate(tabs)) if tabs else np.zeros(1, np.int32)
                 if record is not None:
-                    record("start")
+                    record("start")                 # just before the tc_cycle call
+                    started = True
                 _, out_h = pool.cycle_arrays(hs, uoff, ags, ooff, ids)
                 for a, h, t in zip(ags, out_h, tabs):
                     handles[int(a)] = int(h)
@@ -258,6 +260,8 @@ def run_ours(args):
                 no += int(ooff[-1])
             elif op[0] == "sync":
                 if record is not None:
+                    if not started:                 # a cycle with nothing to move: a zero-length step
+                        record("start")
                     record("end")
                 if retire:
                     pool.sync()
