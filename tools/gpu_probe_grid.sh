@@ -1,4 +1,5 @@
 #!/bin/bash
+# Device-tier probe of the TMA kernel over ring sizes (TC_TMA_RING_KIB) and grids, C2 and C5 geometry.
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 for ring in 64 96; do
   echo "== C2 ring $ring"

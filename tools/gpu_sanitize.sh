@@ -1,4 +1,5 @@
 #!/bin/bash
+# compute-sanitizer memcheck / racecheck / synccheck / initcheck over tools/sanitize_run.py (every kernel path).
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 timeout 1500 python -m pytest tests/test_gpu_parity.py -q -x -k "many_seeds or concatenate" > gpurun_out/pytest_new.log 2>&1; echo "pytest new rc=$?"; tail -3 gpurun_out/pytest_new.log
