@@ -16,7 +16,9 @@ class SetModel:
     def __init__(self, N, S, ncls=2, P=0):
         self.N, self.S, self.P = N, S, P
         self.free = set(range(N))
-        self.pend = []                   # list of (cls, frozenset ids)
+        self.pend = []                   # list of (cls, frozenset ids, epoch)
+        self.ep = 0                      # retire / sync points so far (reading A8')
+        self.back_ep = []                # epoch of each released slot in self.back
         self.own = {}                    # id -> (agent, pos)
         self.tab = {}                    # agent -> list
         self.cls = {}
@@ -75,7 +77,7 @@ class SetModel:
             p = self.own.pop(b)[1]
             pos.append(p)
             self.tab[a][p] = -1
-        self.pend.append((self.cls[a], frozenset(ids)))
+        self.pend.append((self.cls[a], frozenset(ids), self.ep))
         self.nh += 1
         self.live[self.nh] = (a, self.cls[a], pos, slots)
         return self.nh
@@ -93,6 +95,7 @@ class SetModel:
             self.own[b] = (a, p)
             self.tab[a][p] = b
         self.back += slots
+        self.back_ep += [self.ep] * len(slots)
         del self.live[h]
         self.dead.add(h)
         return got
@@ -130,13 +133,27 @@ class SetModel:
         self.clm[c] = max(0, self.clm[c] - len(mine))
 
     def sync(self):
-        for c, ids in self.pend:
-            self.free |= ids
-            self.clm[c] = max(0, self.clm[c] - len(ids))
-        self.pend = []
-        self.stack += [s for s in self.back if s < self.S]
-        self.pstack += [s for s in self.back if s >= self.S]
-        self.back = []
+        self._retire(self.ep + 1)
+
+    def retire(self):
+        self._retire(self.ep)
+
+    def _retire(self, upto):
+        still = []
+        for c, ids, e in self.pend:
+            if e < upto:
+                self.free |= ids
+                self.clm[c] = max(0, self.clm[c] - len(ids))
+            else:
+                still.append((c, ids, e))
+        self.pend = still
+        go = [s for s, e in zip(self.back, self.back_ep) if e < upto]
+        self.stack += [s for s in go if s < self.S]
+        self.pstack += [s for s in go if s >= self.S]
+        keep = [(s, e) for s, e in zip(self.back, self.back_ep) if e >= upto]
+        self.back = [s for s, _ in keep]
+        self.back_ep = [e for _, e in keep]
+        self.ep += 1
 
     def agent_free(self, a):
         if any(v[0] == a for v in self.live.values()):
@@ -150,5 +167,5 @@ class SetModel:
         self.tab[a] = []
 
     def counts(self):
-        npend = sum(len(i) for _, i in self.pend)
+        npend = sum(len(i) for _, i, _ in self.pend)
         return len(self.free), len(self.own), npend

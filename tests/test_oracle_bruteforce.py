@@ -22,6 +22,8 @@ ALPHABET = ([("alloc", a, n) for a in (A, B) for n in (1, 2)]
 assert len(ALPHABET) == 15
 # NEXT-1 gradual reservation: begin a 2-tick reservation for the oldest live handle; one scheduling tick
 ALPHABET_R = ALPHABET + [("reserve_begin", 2), ("tick",)]
+# reading A8': retire without draining (only what was enqueued before the previous retire / sync point)
+ALPHABET_RT = ALPHABET + [("retire",)]
 
 
 def sel_ids(table, sel):
@@ -51,6 +53,8 @@ def run_oracle(p: OraclePool, op):
             return 0, p.reserve_begin(live[0] if live else 0, op[1])
         if k == "tick":
             return 0, p.reserve_tick()
+        if k == "retire":
+            return 0, p.retire()
     except OracleError as e:
         return e.status, None
     raise AssertionError(op)
@@ -78,6 +82,8 @@ def run_model(m: SetModel, op):
             return 0, m.begin(live[0] if live else 0, op[1])
         if k == "tick":
             return 0, m.tick()
+        if k == "retire":
+            return 0, m.retire()
     except Fail as e:
         return e.status, None
     raise AssertionError(op)
@@ -109,7 +115,8 @@ def key(p: OraclePool, m: SetModel):
             tuple(map(tuple, (x[1] for x in p.pending_dev))),
             tuple((h, x.state, tuple(x.pos), tuple(x.slots)) for h, x in p.handles.items()), p.next_handle,
             tuple(sorted(m.free)), tuple(sorted(m.prov.items())), tuple(sorted(m.hprov.items())),
-            tuple(m.stack), tuple(m.pstack), tuple(m.back), tuple(sorted(m.live)),
+            tuple(m.stack), tuple(m.pstack), tuple(m.back), tuple(m.back_ep), m.ep, tuple(sorted(m.live)),
+            tuple(p.pending_epoch), tuple(p.released_epoch), p.epoch,
             tuple((h, tuple(x.plan), x.ticks, tuple(x.resv)) for h, x in p.handles.items()),
             tuple(sorted((h, tuple(v[0]), v[1]) for h, v in m.rplan.items())),
             tuple(sorted((h, tuple(v)) for h, v in m.rsv.items())))
@@ -196,4 +203,12 @@ def test_bruteforce_peer_tier(N, S, P, depth):
     """NEXT-2 peer tier (reading C1): offloads land in the peer slots when the whole offload fits, else in the
     host buffer, else NOHOST; slots return to their own tier at sync."""
     nodes, states = explore(N, S, depth, P=P)
+    assert nodes > 1000 and states > 100
+
+
+@pytest.mark.parametrize("N,S,depth", [(4, 3, 5), (5, 2, 5)])
+def test_bruteforce_retire(N, S, depth):
+    """Every sequence over the 15-op alphabet plus `retire` (A8': retire only what was enqueued before the previous
+    retire / sync point) against the set model with its own epochs."""
+    nodes, states = explore(N, S, depth, alphabet=ALPHABET_RT)
     assert nodes > 1000 and states > 100

@@ -323,3 +323,27 @@ def test_peer_tier_slot_conservation():
                 assert all(x < S for h in p.handles.values() for x in h.slots)
         if P:
             assert any(x >= S for h in p.handles.values() for x in h.slots)
+
+
+def test_retire_without_drain_example():
+    """Reading A8': tests/golden/a8_retire_example.json, hand-derived."""
+    g = gold("a8_retire_example.json")
+    p = OraclePool(g["N"], g["S"], store=ProvStore(g["N"], g["S"]))
+    p.agent_add(0, 0)
+    p.agent_add(1, 0)
+    for st in g["steps"]:
+        if st["op"] == "alloc":
+            assert p.alloc(st["agent"], st["n"]) == st["expect"]
+        elif st["op"] == "offload":
+            p.offload(st["agent"], st["ids"])
+        elif st["op"] == "upload":
+            assert p.upload(st["handle"]) == st["expect"]
+        elif st["op"] == "retire":
+            p.retire()
+        elif st["op"] == "sync":
+            p.sync()
+        s = p.stats()
+        if "expect_free" in st:
+            assert (s["free"], s["pending"]) == (st["expect_free"], st["expect_pending"]), st
+        if "expect_host_free" in st:
+            assert s["host_free"] == st["expect_host_free"], st
