@@ -209,8 +209,14 @@ tc_status tc_query(tc_pool *p, tc_handle h);
 tc_status tc_wait(tc_pool *p, tc_handle h);                        /* host-blocking */
 tc_status tc_stream_wait(tc_pool *p, tc_handle h, void *cuda_stream); /* GPU-side dependency, no host block */
 /* Drain both copy streams; retire PENDING device blocks (FREE, claimed -= min(n, claimed)) in issue order, then
-   return released host slots to the free list.  Uploaded handles are forgotten. */
+   return released host slots to the free list.  Uploaded handles are forgotten.  A retirement point. */
 tc_status tc_sync(tc_pool *p);
+/* Retire without draining (reading A8'; "only returned to the memory pool after the transfer is
+   complete", P:411 asynchronous transfers): waits for, and retires exactly as tc_sync would, only the work enqueued
+   before the previous retirement point (tc_sync or tc_retire); work enqueued since keeps running and stays pending.
+   A serving loop calling tc_retire once per scheduling cycle returns last cycle's blocks and slots while this
+   cycle's transfers stream on.  Ids stay a pure function of the call sequence.  A retirement point. */
+tc_status tc_retire(tc_pool *p);
 
 /* ---- queries ------------------------------------------------------------------------------------------------- */
 tc_status tc_block_table(tc_pool *p, int32_t agent, int32_t *out, int64_t cap, int64_t *n_out); /* -1 = on host */

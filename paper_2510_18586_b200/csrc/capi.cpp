@@ -286,6 +286,14 @@ tc_status tc_stream_wait(tc_pool *p, tc_handle h, void *cuda_stream) {
     TC_CATCH
 }
 
+tc_status tc_retire(tc_pool *p) {
+    TC_GUARD(p) {
+        TC_MUT("tc_retire");
+        return P.retire();
+    }
+    TC_CATCH
+}
+
 tc_status tc_sync(tc_pool *p) {
     TC_GUARD(p) {
         TC_MUT("tc_sync");
@@ -413,11 +421,12 @@ tc_status tc_stats(tc_pool *p, tc_stats_t *s) {
 tc_status tc_timing(tc_pool *p, int32_t enable, tc_timing_t *out) {
     TC_GUARD(p) {
         if (enable < 0 || enable > 2) return TC_E_INVAL;
-        if (!P.meta_only && !P.kts_meta.empty()) {     // kernel stamps are collected lazily (runtime.cpp)
+        if (!P.meta_only && (!P.kts_meta.empty() || !P.spans.empty())) {   // collected lazily (runtime.cpp)
             for (cudaStream_t s : {P.s_up, P.s_off, P.s_up_k, P.s_off_k})
                 if (cudaStreamSynchronize(s) != cudaSuccess) return P.cuda_fail(cudaGetLastError(), "timing sync");
             for (cudaStream_t f : P.foreign)
                 if (cudaStreamSynchronize(f) != cudaSuccess) return P.cuda_fail(cudaGetLastError(), "timing sync");
+            P.spans_collect();
             P.stamps_collect();
         }
         P.timing = P.meta_only ? 0 : enable;

@@ -269,6 +269,8 @@ int32_t Pool::event_get() {
     const int32_t i = ev_free.back();
     ev_free.pop_back();
     ev_used.push_back(i);
+    if ((size_t)i >= ev_epoch.size()) ev_epoch.resize(events.size(), 0);
+    ev_epoch[i] = epoch_id;
     return i;
 }
 
@@ -987,6 +989,7 @@ void Pool::commit_offload(const OffPlan &P, int32_t ev, tc_handle *out) {
             pend.push_back(b);
         }
         pending_dev.emplace_back(ag.cls, std::move(pend));
+        pending_epoch.push_back(epoch_id);
         ++ag.live_offloads;
         const tc_handle h = next_handle++;
         handles.emplace(h, std::move(hr));
@@ -1073,12 +1076,14 @@ void Pool::commit_upload(const UpPlan &P, int32_t ev, int32_t *out_ids) {
             alloc.own_pos[b] = h.pos[q];
             ag.table[h.pos[q]] = b;                        // fused remap's host mirror (A6)
             slots.released.push_back(h.slots[q]);
+            slots.released_epoch.push_back(epoch_id);
             out_ids[i] = b;
         }
         h.resv.clear();
         h.plan.clear();
         resv_active.erase(P.hs[k]);
         h.state = kUploaded;
+        h.up_epoch = epoch_id;
         h.ev = ev;
         --ag.live_offloads;
         ag.up_event = ev;
@@ -1288,44 +1293,87 @@ tc_status Pool::sync() {
         if ((int64_t)kts_meta.size() > kKts / 2) stamps_collect();
         ++sync_count;
     }
-    for (auto &pc : pending_dev) {        // a4 retire in issue order (A10)
-        for (int32_t b : pc.second) {
-            alloc.state[b] = kFree;
-            alloc.set_free(b);
-        }
-        const int64_t k = (int64_t)pc.second.size();
-        alloc.claimed[pc.first] -= std::min(k, alloc.claimed[pc.first]);
+    retire_before(epoch_id + 1);          // everything: the streams are drained
+    return TC_OK;
+}
+
+// tc_retire (reading A8'): wait for and retire only the work enqueued before the previous retirement point — the
+// work of this epoch keeps running.
+tc_status Pool::retire() {
+    if (!meta_only) {
+        if (cuda_dead) return TC_E_CUDA;
+        for (int32_t e : ev_used)
+            if (ev_epoch[e] < epoch_id) TC_CUDA(cudaEventSynchronize(events[e]), "retire wait");
     }
-    pending_dev.clear();
-    // released host slots back to the buffer; pushed in reverse so later pops replay ascending runs
-    for (auto it = slots.released.rbegin(); it != slots.released.rend(); ++it) {
-        if (*it < slots.count) {
-            slots.free_list.push_back(*it);
-            continue;
-        }
-        if (is_peer(*it)) {                                // peer-tier slot: back to its own free list
-            peer.free_list.push_back(*it);
-            continue;
-        }
-        auto sl = std::prev(extra.upper_bound(*it));      // unbuffered ablation: free the slab with its last block
-        if (--sl->second.live == 0) {
-            if (sl->second.host) cudaFreeHost(sl->second.host);
-            extra.erase(sl);
-        }
-    }
-    slots.released.clear();
-    for (auto it = handles.begin(); it != handles.end();) {
-        if (it->second.state == kUploaded) {
-            it = handles.erase(it);
+    retire_before(epoch_id);
+    return TC_OK;
+}
+
+// a4 / a7 bookkeeping for every pending entry, released slot, handle and event created before epoch `upto`, in
+// issue order (A10); then a new epoch starts.  The caller has made sure that work has completed.
+void Pool::retire_before(uint32_t upto) {
+    size_t w = 0;
+    for (size_t i = 0; i < pending_dev.size(); ++i) {
+        if (pending_epoch[i] < upto) {
+            const auto &pc = pending_dev[i];
+            for (int32_t b : pc.second) {
+                alloc.state[b] = kFree;
+                alloc.set_free(b);
+            }
+            const int64_t k = (int64_t)pc.second.size();
+            alloc.claimed[pc.first] -= std::min(k, alloc.claimed[pc.first]);
         } else {
-            it->second.ev = -1;
+            if (w != i) pending_dev[w] = std::move(pending_dev[i]);
+            pending_epoch[w++] = pending_epoch[i];
+        }
+    }
+    pending_dev.resize(w);
+    pending_epoch.resize(w);
+    // released slots back to their buffer; pushed in reverse so later pops replay ascending runs
+    for (size_t i = slots.released.size(); i-- > 0;) {
+        if (slots.released_epoch[i] >= upto) continue;
+        const int64_t x = slots.released[i];
+        if (x < slots.count) {
+            slots.free_list.push_back(x);
+        } else if (is_peer(x)) {                           // peer-tier slot: back to its own free list
+            peer.free_list.push_back(x);
+        } else {
+            auto sl = std::prev(extra.upper_bound(x));    // unbuffered ablation: free the slab with its last block
+            if (--sl->second.live == 0) {
+                if (sl->second.host) cudaFreeHost(sl->second.host);
+                extra.erase(sl);
+            }
+        }
+    }
+    w = 0;
+    for (size_t i = 0; i < slots.released.size(); ++i) {
+        if (slots.released_epoch[i] < upto) continue;
+        slots.released[w] = slots.released[i];
+        slots.released_epoch[w++] = slots.released_epoch[i];
+    }
+    slots.released.resize(w);
+    slots.released_epoch.resize(w);
+    auto retired_ev = [&](int32_t e) { return e >= 0 && ev_epoch[e] < upto; };
+    for (auto it = handles.begin(); it != handles.end();) {
+        if (it->second.state == kUploaded && it->second.up_epoch < upto) {
+            it = handles.erase(it);                        // B3: forgotten once its upload's epoch retires
+        } else {
+            if (retired_ev(it->second.ev)) it->second.ev = -1;
             ++it;
         }
     }
-    for (auto &ag : agents) ag.up_event = -1;
-    for (int32_t e : ev_used) ev_free.push_back(e);
-    ev_used.clear();
-    return TC_OK;
+    for (auto &ag : agents)
+        if (retired_ev(ag.up_event)) ag.up_event = -1;
+    w = 0;
+    for (size_t i = 0; i < ev_used.size(); ++i) {
+        if (ev_epoch[ev_used[i]] < upto) {
+            ev_free.push_back(ev_used[i]);
+        } else {
+            ev_used[w++] = ev_used[i];
+        }
+    }
+    ev_used.resize(w);
+    ++epoch_id;
 }
 
 tc_status Pool::fill(uint64_t seed) {

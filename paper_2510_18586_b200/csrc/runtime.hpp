@@ -47,7 +47,8 @@ struct HostSlots {
     int64_t count = 0;
     int64_t slot_bytes = 0;
     std::vector<int64_t> free_list;  // back() = next slot handed out
-    std::vector<int64_t> released;   // returned to free_list at tc_sync
+    std::vector<int64_t> released;   // returned to free_list at a retirement point (tc_sync / tc_retire)
+    std::vector<uint32_t> released_epoch;   // retirement epoch each released slot was created in
 };
 
 // NEXT-2 peer tier: block-shard slots in a neighbouring GPU's HBM, ids S .. S+count-1, own LIFO free list.
@@ -75,6 +76,7 @@ struct HandleRec {
     std::vector<int64_t> plan;       // gradual reservation: chunk per tick (empty = none active)
     int32_t ticks = 0;
     std::vector<int32_t> resv;       // destination blocks claimed so far, in claim order
+    uint32_t up_epoch = 0;           // retirement epoch of its upload (forgotten once that epoch retires)
 };
 
 struct Pool {
@@ -129,6 +131,11 @@ struct Pool {
     std::unordered_map<uint64_t, HandleRec> handles;
     uint64_t next_handle = 1;
     std::vector<std::pair<int32_t, std::vector<int32_t>>> pending_dev;   // (cls, ids) in issue order
+    std::vector<uint32_t> pending_epoch;     // retirement epoch of each pending entry (reading A8')
+    uint32_t epoch_id = 0;                   // retirement points (tc_sync / tc_retire) so far
+    std::vector<uint32_t> ev_epoch;          // per event index: the epoch it was last handed out in
+    tc_status retire();                      // tc_retire: retire what was enqueued before the previous point
+    void retire_before(uint32_t upto);
     std::vector<uint32_t> stamp;
     uint32_t epoch = 0;
 

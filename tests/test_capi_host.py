@@ -57,7 +57,7 @@ def replay_both(ops, N, S, ncls=N_CLASSES, max_bpa=4096, P=0):
     for i, op in enumerate(ops):
         a, b = ro.step(op), rc.step(op)
         assert a == b, (i, op, a, b)
-        if op[0] in ("sync", "upload_batch", "offload_batch"):
+        if op[0] in ("sync", "retire", "upload_batch", "offload_batch"):
             assert stats_view(o.stats()) == stats_view(c.stats()), (i, op)
     for ag in o.agents:
         assert o.block_table(ag) == c.block_table(ag)
@@ -243,3 +243,15 @@ def test_header_is_plain_c_and_demo_runs(tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stderr
     assert r.stdout.startswith("ok: 48 blocks")
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_fuzz_scripts_with_retire_match_oracle(seed, monkeypatch):
+    """Reading A8' through the C ABI: scripts mixing tc_retire (retire only what was enqueued before the previous
+    retirement point) with syncs, cycles, gradual reservations and the peer tier; TC_CHECK on."""
+    monkeypatch.setenv("TC_CHECK", "1")
+    rng = np.random.default_rng(2000 + seed)
+    N, S, P = int(rng.choice([24, 64])), int(rng.choice([6, 16])), int(rng.choice([0, 4]))
+    ops = fuzz_script(700 + seed, n_ops=200, n_agents=3, n_classes=2, N=N, max_alloc=6, gradual=seed % 2 == 0,
+                      retire=True)
+    replay_both(ops, N, S, ncls=2, P=P)

@@ -490,3 +490,36 @@ def test_long_random_stream_with_invariant_checks(monkeypatch, mode, P):
     L, H, D, N, S, T = 3, 2, 64, 50, 20, 16
     ops = fuzz_script(4242 + P, n_ops=8000, n_agents=4, n_classes=2, N=N, max_alloc=6, gradual=True)
     run_script(ops, L, H, D, N, S, mode, ncls=2, seed=9, staging=3 * 2 * L * T * H * D * 2, T=T, P=P)
+
+
+@pytest.mark.parametrize("mode", ["auto", "staged", "direct", "staged_tile"])
+def test_retire_without_drain_bytes(mode):
+    """Reading A8' on the GPU: tc_retire returns last epoch's blocks and slots while this epoch's transfers are
+    still streaming; the next transfers reuse them.  Whole pool, host images, tables and counters equal the oracle
+    after every sync, on scripts that retire often and sync rarely."""
+    L, H, D, N, S, T = 4, 4, 128, 40, 24, 16
+    for seed in range(3):
+        ops = [op for op in fuzz_script(seed + 90, n_ops=150, n_agents=3, n_classes=2, N=N, max_alloc=6,
+                                        gradual=True, retire=True) if op[0] != "sync" or seed == 0]
+        ops.append(("sync",))
+        run_script(ops, L, H, D, N, S, mode, ncls=2, seed=seed + 11, T=T)
+
+
+def test_retire_keeps_this_epochs_transfer_running():
+    """tc_retire does not wait for work enqueued after the previous retirement point: with a large offload in
+    flight, retire() leaves its blocks pending (and normally returns while it still streams); a second retire
+    then returns them."""
+    L, H, D, N, S = 28, 4, 128, 1024, 512             # C2-shaped blocks; 400 blocks ~ 360 MB ~ 7 ms over PCIe
+    c = tcb.Pool(L, H, D, 16, "bf16", N, device=0, host_slots=S, xfer_d2h=tcb.XFER_STAGED, xfer_h2d=tcb.XFER_STAGED)
+    c.fill(3)
+    c.agent_add(0, 0)
+    c.alloc(0, 400)
+    c.retire()                                        # a retirement point before the offload
+    h = c.offload(0, c.block_table(0))
+    c.retire()                                        # must not drain the offload enqueued after the last point
+    busy = not c.query(h)                             # normally still streaming (~7 ms over PCIe)
+    assert c.stats()["pending"] == 400                # not retired either way: enqueued after the previous point
+    print("offload still in flight after retire():", busy)
+    c.retire()
+    assert c.stats()["pending"] == 0 and c.stats()["free"] == N
+    c.close()

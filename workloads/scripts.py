@@ -136,12 +136,13 @@ def c1_worked_example() -> list:
 
 
 def fuzz_script(seed: int, n_ops: int = 60, n_agents: int = 3, n_classes: int = 2, N: int = 64,
-                max_alloc: int = 6, p_err: float = 0.05, gradual: bool = False) -> list:
+                max_alloc: int = 6, p_err: float = 0.05, gradual: bool = False, retire: bool = False) -> list:
     """Random op mix for small pools, including error paths (bad ids, double uploads, over-quota, BUSY frees)."""
     rng = np.random.default_rng(seed)
     ops = [("agent_add", a, a % n_classes) for a in range(n_agents)]
     kinds = ["alloc", "alloc", "offload", "offload_some", "upload", "sync", "reserve", "agent_free",
-             "offload_batch", "upload_batch", "cycle"] + (["reserve_begin", "tick", "tick", "reserve_cancel"] if gradual else [])
+             "offload_batch", "upload_batch", "cycle"] + (["reserve_begin", "tick", "tick", "reserve_cancel"] if gradual else []) \
+        + (["retire", "retire"] if retire else [])
     for _ in range(n_ops):
         k = kinds[rng.integers(len(kinds))]
         a = int(rng.integers(n_agents))
@@ -173,6 +174,8 @@ def fuzz_script(seed: int, n_ops: int = 60, n_agents: int = 3, n_classes: int = 
             ops.append(("reserve_begin", a, int(rng.integers(1, 4))))
         elif k == "tick":
             ops.append(("tick",))
+        elif k == "retire":
+            ops.append(("retire",))
         else:
             ops.append(("reserve_cancel", a))
         if rng.random() < p_err:
