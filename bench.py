@@ -1,10 +1,12 @@
 #!/usr/bin/env python
 """Benchmark of the Tokencake offload/upload hot path on B200 (one process per GPU).
 
-A *step* is one scheduling cycle of the whole hot path: the cycle's uploads of agents
-whose function call is over (a5 allocation + a6 H2D scatter with the fused table remap), then the cycle's offloads of
-agents entering a function call (a2 admission + a3 gather/D2H), then the sync that retires pending blocks and returns
-host slots (a4, a7) — exactly the P:645-648 order, through the C ABI.
+A *step* is one scheduling cycle of the whole hot path through the C ABI, in the
+P:645-648 order: the cycle's uploads of agents whose function call is over (a5 allocation + a6 H2D scatter with the
+fused table remap), then the cycle's offloads of agents entering a function call (a2 admission + a3 gather/D2H), then
+its retirement point (a4, a7).  By default the retirement is tc_retire — the previous cycle's transfers return their
+blocks and slots while this cycle's stream on, the asynchronous loop of P:645-648 (reading A8'); --retire sync drains
+every cycle with tc_sync instead (that number is also reported, as `per_cycle_drain`).
 
   python bench.py [--gpus N --steps K --warmup W] [--workload c2|c3|c4|c5] [--mode auto|direct|staged]
   python bench.py --impl reference ...     # the CPU oracle (oracle/), timed on the host cores
@@ -52,6 +54,10 @@ def parse():
                          "HBM when it is alone); offloads go there first")
     ap.add_argument("--trace", default=None, metavar="FILE",
                     help="write the per-call trace (tc_trace) of the diagnostic steps as JSONL")
+    ap.add_argument("--retire", default="each", choices=["each", "sync"],
+                    help="each: every step is tc_cycle + tc_retire (retire the previous cycle's transfers without "
+                         "draining this one's: the asynchronous loop of P:645-648); sync: tc_cycle + tc_sync "
+                         "(drain every step)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--quick", action="store_true", help="skip host-link probe and device-tier microbench")
@@ -233,9 +239,10 @@ def run_ours(args):
     gen = CycleGen(cfg, agents, combined=True)
     handles, sizes = {}, {}
 
-    def cycle(record=None, retire=True):
-        """One scheduling cycle through the public API (tc_cycle: uploads then offloads, then tc_sync — skipped when
-        retire is False); returns (blocks_up, blocks_off)."""
+    def cycle(record=None, retire="sync"):
+        """One scheduling cycle through the public API (tc_cycle: uploads then offloads), then its retirement point:
+        retire = "sync" (tc_sync: drain and retire everything) or "retire" (tc_retire: retire what was enqueued
+        before the previous point); returns (blocks_up, blocks_off)."""
         nu = no = 0
         started = False
         for op in gen.next_cycle():
@@ -263,8 +270,10 @@ def run_ours(args):
                     if not started:                 # a cycle with nothing to move: a zero-length step
                         record("start")
                     record("end")
-                if retire:
+                if retire == "sync":
                     pool.sync()
+                else:
+                    pool.retire()
         return nu, no
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
@@ -286,7 +295,29 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     dev_ms, host_ms, bytes_up, bytes_off, blocks, step_bytes = [], [], 0, 0, 0, []
     t_wall0 = time.perf_counter()
-    for _ in range(args.steps):
+    if args.retire == "each":
+        # the asynchronous loop: each step enqueues its cycle and retires the previous one's transfers
+        # (tc_retire) without draining its own, so consecutive cycles stream back to back; the last cycle is drained
+        # by a tc_sync inside the timed region.  Device time = first step's start -> last step's end on both copy
+        # streams.  No L2 flush: each step streams ~2x the 126 MB L2 through blocks the previous steps did not touch.
+        e0 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        e1 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        for e, st in zip(e0, (ups, offs_)):
+            e.record(st)
+        for k in range(args.steps):
+            nu, no = cycle(retire="retire")
+            step_bytes.append((nu * B, no * B))
+            bytes_up += nu * B
+            bytes_off += no * B
+            blocks += nu + no
+        for e, st in zip(e1, (ups, offs_)):
+            e.record(st)
+        pool.sync()
+        torch.cuda.synchronize(dev)
+        total_ms = max(e0[a].elapsed_time(e1[b]) for a in range(2) for b in range(2))
+        dev_ms = [total_ms / args.steps] * args.steps
+        host_ms = [(time.perf_counter() - t_wall0) * 1e3 / args.steps] * args.steps
+    for _ in range(args.steps if args.retire == "sync" else 0):
         flush.zero_()                          # flush L2 between steps (outside the step's events)
         torch.cuda.synchronize(dev)
         ev = {}
@@ -297,7 +328,7 @@ def run_ours(args):
             for nm, st in pair:
                 e = torch.cuda.Event(enable_timing=True); e.record(st); ev[nm] = e
         t0 = time.perf_counter()                # host clock (e2e): the whole public-API cycle incl. id lookups
-        nu, no = cycle(record)
+        nu, no = cycle(record, retire="sync")
         t1 = time.perf_counter()
         ref = ev["up0"]
         start = min(0.0, ref.elapsed_time(ev["off0"]))
@@ -331,7 +362,8 @@ def run_ours(args):
                 f.write(json.dumps(r) + "\n")
     diag = pool.timing(0)
     tl_raw = pool.timeline(200000)
-    steady = steady_state(torch, dev, cycle, ups, offs_, B, min(args.steps, 40), pool, step_bytes, cfg.stall_cycles)
+    other = per_cycle_drain(torch, dev, cycle, ups, offs_, B, min(args.steps, 40), flush) if args.retire == "each" \
+        else None
     tl_summary = timeline_summary(tl_raw)
     if os.environ.get("TC_DUMP_TIMELINE"):                 # debugging aid: raw per-span records of the diagnostic steps
         with open(os.environ["TC_DUMP_TIMELINE"], "w") as f:
@@ -407,14 +439,20 @@ def run_ours(args):
     if link and not args.peer:
         bi = link["bidir_gbs"] / 2
         tmin = 0.0
-        for u, o in step_bytes:
-            lo, hi = min(u, o), max(u, o)
-            uni = link["h2d_gbs"] if u >= o else link["d2h_gbs"]
-            tmin += lo / (bi * 1e9) + (hi - lo) / (uni * 1e9)
+        if args.retire == "each":              # steps stream back to back: the bound is on the totals
+            up, off = sum(u for u, _ in step_bytes), sum(o for _, o in step_bytes)
+            tmin = max(up / (link["h2d_gbs"] * 1e9), off / (link["d2h_gbs"] * 1e9), (up + off) / (link["bidir_gbs"] * 1e9))
+            how = ("all steps: max(total up / H2D peak, total off / D2H peak, total / bidirectional peak), the link's "
+                   "lower bound for any schedule, vs the measured time")
+        else:
+            for u, o in step_bytes:
+                lo, hi = min(u, o), max(u, o)
+                uni = link["h2d_gbs"] if u >= o else link["d2h_gbs"]
+                tmin += lo / (bi * 1e9) + (hi - lo) / (uni * 1e9)
+            how = ("per step: min(up,off) at half the measured bidirectional peak + the excess at the unidirectional "
+                   "peak, vs the measured step time")
         link_roof = {"bound": "host_link", "step_min_ms": tmin * 1e3 / len(step_bytes),
-                     "step_ms": sum(dev_ms) / len(dev_ms), "frac": tmin * 1e3 / sum(dev_ms),
-                     "how": "per step: min(up,off) at half the measured bidirectional peak + the excess at the "
-                            "unidirectional peak, vs the measured step time"}
+                     "step_ms": sum(dev_ms) / len(dev_ms), "frac": tmin * 1e3 / sum(dev_ms), "how": how}
         for k, pk in (("memcpy_d2h", "d2h_gbs"), ("memcpy_h2d", "h2d_gbs")):
             if k in kern:
                 link_roof[k + "_frac_of_unidir_peak"] = kern[k]["achieved_gbs"] / link[pk]
@@ -431,7 +469,12 @@ def run_ours(args):
                    "block_tokens": cfg.T, "head_shards": G, "n_blocks": cfg.N, "block_shard_bytes": B,
                    "host_slots": S, "agents": cfg.n_agents, "per_cycle": cfg.per_cycle,
                    "xfer": XFER_NAMES[stats["xfer_d2h"]] + "/" + XFER_NAMES[stats["xfer_h2d"]],
-                   "l2": "flushed between steps (256 MiB write, outside the step events)",
+                   "l2": ("not flushed: every step streams ~2x the 126 MB L2 through blocks the previous steps did "
+                          "not touch" if args.retire == "each" else
+                          "flushed between steps (256 MiB write, outside the step events)"),
+                   "step": ("tc_cycle + tc_retire (retire the previous cycle's transfers, do not drain this one's); "
+                            "a tc_sync drains the last cycle inside the timed region" if args.retire == "each" else
+                            "tc_cycle + tc_sync (drain and retire every cycle)"),
                    "parallelism": f"{world} independent ranks" + (f", head-sharded G={G}" if G > 1 else ""),
                    "numa": numa,
                    "offload_tier": ("peer slots on GPU %d (%s) first, then host" % (
@@ -448,7 +491,7 @@ def run_ours(args):
             "how": "sum of the transfer kernels' device durations / the steps' device time: the fraction of the step "
                    "during which this path occupies SMs (the copy-engine DMAs use none); rank 0"},
         "timeline": tl_summary,
-        "steady_state": steady,
+        "per_cycle_drain": other,
         "hostlink_peak": link,
         "roofline": roof,
         "roofline_link": link_roof,
@@ -483,37 +526,28 @@ def ncu_traffic(cfg_name, kind, kd):
                                "note": "ncu counts writes still dirty in L2 at kernel end as not yet written"}}
 
 
-def steady_state(torch, dev, cycle, ups, offs, B, n, pool, step_bytes, stall_cycles):
-    """Diagnostic (not `value`): the same cycles enqueued back to back and retired (tc_sync) only every k cycles, as
-    a serving loop that does not drain the copy streams each cycle would run them — the host link then stays busy
-    across cycle boundaries.  k (<= 4) is the most cycles the pool's free blocks and host slots can carry without
-    retirement, judged from the timed steps' largest batches; k = 1 means no pipelining fits.  Device time from the
-    first cycle's start to the last one's end on both copy streams."""
-    s = pool.stats()
-    up_max = max(u for u, _ in step_bytes) // B
-    off_max = max(o for _, o in step_bytes) // B
-    k = 1
-    for kk in (4, 3, 2):
-        if s["free"] >= kk * up_max + off_max and s["host_free"] >= (kk + stall_cycles + 1) * off_max:
-            k = kk
-            break
-    torch.cuda.synchronize(dev)
-    e0 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    e1 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    for e, s in zip(e0, (ups, offs)):
-        e.record(s)
-    moved = 0
-    for i in range(n):
-        last = i == n - 1
-        nu, no = cycle(retire=(i + 1) % k == 0 and not last)
+def per_cycle_drain(torch, dev, cycle, ups, offs, B, n, flush):
+    """Diagnostic (not `value`): the same cycles run with a tc_sync each (drain and retire every cycle, L2 flushed
+    between them); device time per cycle from just before tc_cycle to the end of both copy streams' work."""
+    tot_ms, moved = 0.0, 0
+    for _ in range(n):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        ev = {}
+
+        def record(tag):
+            for nm, st in ((tag + "u", ups), (tag + "o", offs)):
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(st)
+                ev[nm] = e
+        nu, no = cycle(record, retire="sync")
+        if "startu" not in ev:
+            continue
+        tot_ms += max(ev["startu"].elapsed_time(ev["endu"]), ev["startu"].elapsed_time(ev["endo"]),
+                      ev["starto"].elapsed_time(ev["endu"]), ev["starto"].elapsed_time(ev["endo"]))
         moved += (nu + no) * B
-        if last:
-            for e, s in zip(e1, (ups, offs)):
-                e.record(s)
-    pool.sync()
-    ms = max(e0[a].elapsed_time(e1[b]) for a in range(2) for b in range(2))
-    return {"value": moved / (ms * 1e-3) / 1e9, "unit": "GB/s", "cycles": n, "sync_every": k,
-            "how": "cycles enqueued back to back, tc_sync every k cycles; bytes both directions / device time"}
+    return {"value": moved / (tot_ms * 1e-3) / 1e9 if tot_ms else None, "unit": "GB/s", "cycles": n,
+            "how": "tc_cycle + tc_sync per cycle (drained), L2 flushed between cycles"}
 
 
 def timeline_summary(spans):

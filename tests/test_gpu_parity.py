@@ -189,7 +189,9 @@ def test_full_size_config_parity(name, world):
     cfg = CONFIGS[name]
     rank = world - 1 if world > 1 else 0
     S = cfg.host_slots()
-    ops = build_script(cfg, 8, combined=True)          # tc_cycle per scheduling cycle, as bench.py times it
+    ops = build_script(cfg, 8, combined=True)          # tc_cycle + tc_retire per scheduling cycle, as bench.py times it
+    n_setup = next(i for i, op in enumerate(ops) if op[0] == "cycle")
+    ops = ops[:n_setup] + [("retire",) if op[0] == "sync" else op for op in ops[n_setup:]] + [("sync",)]
     o = OraclePool(cfg.N, S, max_agents=1024, max_blocks_per_agent=cfg.max_blocks_per_agent,
                    store=ProvStore(cfg.N, S))
     c = tcb.Pool(cfg.L, cfg.H, cfg.D, cfg.T, cfg.dtype, cfg.N, device=0, shard_rank=rank, shard_world=world,
