@@ -239,6 +239,8 @@ def run_ours(args):
     gen = CycleGen(cfg, agents, combined=True)
     handles, sizes = {}, {}
 
+    drains = [0]
+
     def cycle(record=None, retire="sync"):
         """One scheduling cycle through the public API (tc_cycle: uploads then offloads), then its retirement point:
         retire = "sync" (tc_sync: drain and retire everything) or "retire" (tc_retire: retire what was enqueued
@@ -259,7 +261,14 @@ def run_ours(args):
                 if record is not None:
                     record("start")                 # just before the tc_cycle call
                     started = True
-                _, out_h = pool.cycle_arrays(hs, uoff, ags, ooff, ids)
+                try:
+                    _, out_h = pool.cycle_arrays(hs, uoff, ags, ooff, ids)
+                except tcb.TcError as e:            # refused, nothing changed (host buffer / blocks held by the
+                    if e.status not in (tcb.E_NOHOST, tcb.E_NOBLOCKS) or retire == "sync":   # undrained cycles):
+                        raise                                                              # drain and retry once
+                    pool.sync()
+                    drains[0] += 1
+                    _, out_h = pool.cycle_arrays(hs, uoff, ags, ooff, ids)
                 for a, h, t in zip(ags, out_h, tabs):
                     handles[int(a)] = int(h)
                     sizes[int(h)] = len(t)
@@ -304,6 +313,7 @@ def run_ours(args):
         e1 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         for e, st in zip(e0, (ups, offs_)):
             e.record(st)
+        drains[0] = 0
         for k in range(args.steps):
             nu, no = cycle(retire="retire")
             step_bytes.append((nu * B, no * B))
@@ -473,7 +483,9 @@ def run_ours(args):
                           "not touch" if args.retire == "each" else
                           "flushed between steps (256 MiB write, outside the step events)"),
                    "step": ("tc_cycle + tc_retire (retire the previous cycle's transfers, do not drain this one's); "
-                            "a tc_sync drains the last cycle inside the timed region" if args.retire == "each" else
+                            "a cycle the host buffer / free blocks refuse is retried once after a tc_sync "
+                            f"({drains[0]} of {n_steps} steps needed it); a tc_sync drains the last cycle inside the "
+                            "timed region" if args.retire == "each" else
                             "tc_cycle + tc_sync (drain and retire every cycle)"),
                    "parallelism": f"{world} independent ranks" + (f", head-sharded G={G}" if G > 1 else ""),
                    "numa": numa,

@@ -255,3 +255,15 @@ def test_fuzz_scripts_with_retire_match_oracle(seed, monkeypatch):
     ops = fuzz_script(700 + seed, n_ops=200, n_agents=3, n_classes=2, N=N, max_alloc=6, gradual=seed % 2 == 0,
                       retire=True)
     replay_both(ops, N, S, ncls=2, P=P)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+def test_config_scripts_retire_each_match_oracle(name):
+    """bench.py's default loop at full size: tc_cycle + tc_retire per cycle, a refused cycle retried once after a
+    tc_sync (cycle_r) — identical statuses, ids, handles, tables and counters to the oracle (metadata-only pool)."""
+    cfg = CONFIGS[name]
+    ops = build_script(cfg, 8, combined=True)
+    n_setup = next(i for i, op in enumerate(ops) if op[0] == "cycle")
+    ops = ops[:n_setup] + [("retire",) if op[0] == "sync" else ("cycle_r",) + op[1:] if op[0] == "cycle" else op
+                           for op in ops[n_setup:]] + [("sync",)]
+    o, c = replay_both(ops, cfg.N, cfg.host_slots(), max_bpa=cfg.max_blocks_per_agent)

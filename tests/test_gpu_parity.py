@@ -191,7 +191,8 @@ def test_full_size_config_parity(name, world):
     S = cfg.host_slots()
     ops = build_script(cfg, 8, combined=True)          # tc_cycle + tc_retire per scheduling cycle, as bench.py times it
     n_setup = next(i for i, op in enumerate(ops) if op[0] == "cycle")
-    ops = ops[:n_setup] + [("retire",) if op[0] == "sync" else op for op in ops[n_setup:]] + [("sync",)]
+    ops = ops[:n_setup] + [("retire",) if op[0] == "sync" else ("cycle_r",) + op[1:] if op[0] == "cycle" else op
+                           for op in ops[n_setup:]] + [("sync",)]
     o = OraclePool(cfg.N, S, max_agents=1024, max_blocks_per_agent=cfg.max_blocks_per_agent,
                    store=ProvStore(cfg.N, S))
     c = tcb.Pool(cfg.L, cfg.H, cfg.D, cfg.T, cfg.dtype, cfg.N, device=0, shard_rank=rank, shard_world=world,
@@ -203,7 +204,7 @@ def test_full_size_config_parity(name, world):
         a, b = ro.step(op), rc.step(op)
         assert a == b, (i, op)
         assert a[0] == 0, (i, op)
-        if op[0] == "cycle" and a[1]:
+        if op[0] in ("cycle", "cycle_r") and a[1]:
             for ids in a[1][0]:
                 touched.update(ids)
     c.sync()

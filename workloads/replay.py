@@ -65,7 +65,9 @@ class Replayer:
                 out = [list(x) for x in p.upload_batch(hs)]
                 for a in op[1]:
                     self.handles[a].popleft()
-            elif kind == "cycle":                # ("cycle", [upload agents], [(agent, sel), ...])
+            elif kind in ("cycle", "cycle_r"):   # ("cycle", [upload agents], [(agent, sel), ...])
+                # cycle_r: a refused cycle (no host slots / device blocks: nothing changed) is retried once after a
+                # tc_sync — the caller policy of bench.py's retire-each loop ("the caller retries")
                 items = [(a, self._ids(a, sel)) for a, sel in op[2]]       # resolved on pre-cycle tables
                 taken = defaultdict(int)
                 hs = []
@@ -73,7 +75,13 @@ class Replayer:
                     q = self.handles.get(a, ())
                     hs.append(q[taken[a]] if taken[a] < len(q) else 0)
                     taken[a] += 1
-                news, out_h = p.cycle(hs, items)
+                try:
+                    news, out_h = p.cycle(hs, items)
+                except Exception as e:  # noqa: BLE001
+                    if kind != "cycle_r" or getattr(e, "status", None) not in (-2, -3):
+                        raise
+                    p.sync()
+                    news, out_h = p.cycle(hs, items)
                 for a in op[1]:
                     self.handles[a].popleft()
                 for (a, _), h in zip(op[2], out_h):
