@@ -54,10 +54,11 @@ def parse():
                          "HBM when it is alone); offloads go there first")
     ap.add_argument("--trace", default=None, metavar="FILE",
                     help="write the per-call trace (tc_trace) of the diagnostic steps as JSONL")
-    ap.add_argument("--retire", default="each", choices=["each", "sync"],
+    ap.add_argument("--retire", default="auto", choices=["auto", "each", "sync"],
                     help="each: every step is tc_cycle + tc_retire (retire the previous cycle's transfers without "
                          "draining this one's: the asynchronous loop of P:645-648); sync: tc_cycle + tc_sync "
-                         "(drain every step)")
+                         "(drain every step); auto: each when the pool's host buffer and free blocks can carry a "
+                         "second cycle in flight (judged from the warm-up cycles), else sync")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--quick", action="store_true", help="skip host-link probe and device-tier microbench")
@@ -292,8 +293,15 @@ def run_ours(args):
     clocks = Clocks(local)                     # sampled from warm-up through the end of the timed region
     for _ in range(cfg.stall_cycles + 1):      # prime: get stalled agents to upload
         cycle()
-    for _ in range(args.warmup):
-        cycle()
+    warm = [cycle() for _ in range(max(args.warmup, 3))]
+    if args.retire == "auto":                  # room for one more cycle in flight than a drained loop needs?
+        s = pool.stats()
+        up_max = max(u for u, _ in warm)
+        off_max = max(o for _, o in warm)
+        # retire-each keeps one more cycle of host slots (released by uploads) and of pending source blocks
+        # (offloads) unreturned than a drained loop does; 10 % margin over the warm-up's largest cycle
+        fits = s["host_free"] >= 2.2 * off_max and s["free"] >= 1.1 * (up_max + 2 * off_max)
+        args.retire = "each" if fits else "sync"
     # timed region: the kernels' own %globaltimer start/end only (timing mode 2: no extra events on the streams)
     pool.timing(2)
     pool.timing(2)                             # reset accumulators
