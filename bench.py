@@ -143,7 +143,7 @@ def bind_numa_local(index: int) -> str:
         return f"unbound ({type(e).__name__})"
 
 
-def hostlink_peak(torch, dev, nbytes=1 << 30, reps=5):
+def hostlink_peak(torch, dev, nbytes=1 << 30, reps=10):
     """Pinned cudaMemcpyAsync D2H / H2D / bidirectional, best of `reps`."""
     h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
     h2 = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
@@ -171,7 +171,7 @@ def hostlink_peak(torch, dev, nbytes=1 << 30, reps=5):
 
     r = {"h2d_gbs": best(lambda: d.copy_(h, non_blocking=True), nbytes),
          "d2h_gbs": best(lambda: h.copy_(d, non_blocking=True), nbytes),
-         "bidir_gbs": best(bidir, 2 * nbytes), "bytes": nbytes, "how": "torch pinned copy_ 1 GiB, best of 5"}
+         "bidir_gbs": best(bidir, 2 * nbytes), "bytes": nbytes, "how": "torch pinned copy_ 1 GiB, best of 10"}
     del h, h2, d, d2
     return r
 
