@@ -372,8 +372,13 @@ def run_ours(args):
     if args.trace:
         pool.trace(100000)
     n_diag = min(args.steps, 20)
+    # TC_DIAG_RETIRE=1: run the diagnostic cycles in the timed loop's retire-each form (one timeline over all of
+    # them, for TC_DUMP_TIMELINE / tools/timeline_gaps.py) instead of drained
+    diag_each = args.retire == "each" and os.environ.get("TC_DIAG_RETIRE") == "1"
     for _ in range(n_diag):
-        cycle()
+        cycle(retire="retire" if diag_each else "sync")
+    if diag_each:
+        pool.sync()
     if args.trace and rank == 0:
         with open(args.trace, "w") as f:
             for r in pool.trace_read(100000):

@@ -135,8 +135,10 @@ class SetModel:
     def sync(self):
         self._retire(self.ep + 1)
 
-    def retire(self):
-        self._retire(self.ep)
+    def retire(self, lag=1):
+        if lag < 1:
+            raise Fail(INVAL)
+        self._retire(max(0, self.ep - (lag - 1)))
 
     def _retire(self, upto):
         still = []

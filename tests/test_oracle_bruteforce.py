@@ -24,6 +24,8 @@ assert len(ALPHABET) == 15
 ALPHABET_R = ALPHABET + [("reserve_begin", 2), ("tick",)]
 # reading A8': retire without draining (only what was enqueued before the previous retire / sync point)
 ALPHABET_RT = ALPHABET + [("retire",)]
+# reading A8'': retire against the lag-th previous point (lag 2), and the refused lag 0
+ALPHABET_RL = ALPHABET + [("retire",), ("retire", 2), ("retire", 0)]
 
 
 def sel_ids(table, sel):
@@ -54,7 +56,7 @@ def run_oracle(p: OraclePool, op):
         if k == "tick":
             return 0, p.reserve_tick()
         if k == "retire":
-            return 0, p.retire()
+            return 0, p.retire(*op[1:])
     except OracleError as e:
         return e.status, None
     raise AssertionError(op)
@@ -83,7 +85,7 @@ def run_model(m: SetModel, op):
         if k == "tick":
             return 0, m.tick()
         if k == "retire":
-            return 0, m.retire()
+            return 0, m.retire(*op[1:])
     except Fail as e:
         return e.status, None
     raise AssertionError(op)
@@ -211,4 +213,12 @@ def test_bruteforce_retire(N, S, depth):
     """Every sequence over the 15-op alphabet plus `retire` (A8': retire only what was enqueued before the previous
     retire / sync point) against the set model with its own epochs."""
     nodes, states = explore(N, S, depth, alphabet=ALPHABET_RT)
+    assert nodes > 1000 and states > 100
+
+
+@pytest.mark.parametrize("N,S,depth", [(4, 3, 5), (5, 2, 5)])
+def test_bruteforce_retire_lag(N, S, depth):
+    """Every sequence over the 15-op alphabet plus retire with lag 1, 2 and the refused 0 (reading A8'': retire only
+    what was enqueued before the lag-th previous retirement point) against the set model with its own epochs."""
+    nodes, states = explore(N, S, depth, alphabet=ALPHABET_RL)
     assert nodes > 1000 and states > 100

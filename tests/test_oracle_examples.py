@@ -347,3 +347,32 @@ def test_retire_without_drain_example():
             assert (s["free"], s["pending"]) == (st["expect_free"], st["expect_pending"]), st
         if "expect_host_free" in st:
             assert s["host_free"] == st["expect_host_free"], st
+
+
+def test_retire_lag_example():
+    """Reading A8'': tests/golden/a8_retire_lag_example.json, hand-derived (retire against the lag-th
+    previous retirement point; lag 0 refused with no change)."""
+    g = gold("a8_retire_lag_example.json")
+    p = OraclePool(g["N"], g["S"], store=ProvStore(g["N"], g["S"]))
+    for a in range(3):
+        p.agent_add(a, 0)
+    for st in g["steps"]:
+        try:
+            if st["op"] == "alloc":
+                assert p.alloc(st["agent"], st["n"]) == st["expect"]
+            elif st["op"] == "offload":
+                p.offload(st["agent"], st["ids"])
+            elif st["op"] == "upload":
+                assert p.upload(st["handle"]) == st["expect"]
+            elif st["op"] == "retire":
+                p.retire(st.get("lag", 1))
+            elif st["op"] == "sync":
+                p.sync()
+            assert "expect_error" not in st, st
+        except OracleError as e:
+            assert st.get("expect_error") == "INVAL" and e.status == E_INVAL, st
+        s = p.stats()
+        if "expect_free" in st:
+            assert (s["free"], s["pending"]) == (st["expect_free"], st["expect_pending"]), st
+        if "expect_host_free" in st:
+            assert s["host_free"] == st["expect_host_free"], st

@@ -89,8 +89,8 @@ class Replayer:
                 out = ([list(x) for x in news], list(out_h))
             elif kind == "sync":
                 p.sync(); out = None
-            elif kind == "retire":
-                p.retire(); out = None
+            elif kind == "retire":             # ("retire",) or ("retire", lag) (readings A8', A8'')
+                p.retire(*op[1:]); out = None
             elif kind == "agent_free":
                 p.agent_free(op[1]); out = None
             elif kind == "reserve_begin":        # gradual reservation for the agent's oldest handle (NEXT-1)

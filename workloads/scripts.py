@@ -136,7 +136,8 @@ def c1_worked_example() -> list:
 
 
 def fuzz_script(seed: int, n_ops: int = 60, n_agents: int = 3, n_classes: int = 2, N: int = 64,
-                max_alloc: int = 6, p_err: float = 0.05, gradual: bool = False, retire: bool = False) -> list:
+                max_alloc: int = 6, p_err: float = 0.05, gradual: bool = False, retire: bool = False,
+                lags: tuple = (1,)) -> list:
     """Random op mix for small pools, including error paths (bad ids, double uploads, over-quota, BUSY frees)."""
     rng = np.random.default_rng(seed)
     ops = [("agent_add", a, a % n_classes) for a in range(n_agents)]
@@ -175,7 +176,8 @@ def fuzz_script(seed: int, n_ops: int = 60, n_agents: int = 3, n_classes: int = 
         elif k == "tick":
             ops.append(("tick",))
         elif k == "retire":
-            ops.append(("retire",))
+            lag = int(lags[rng.integers(len(lags))])
+            ops.append(("retire",) if lag == 1 else ("retire", lag))
         else:
             ops.append(("reserve_cancel", a))
         if rng.random() < p_err:
