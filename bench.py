@@ -4,9 +4,10 @@
 A *step* is one scheduling cycle of the whole hot path through the C ABI, in the
 P:645-648 order: the cycle's uploads of agents whose function call is over (a5 allocation + a6 H2D scatter with the
 fused table remap), then the cycle's offloads of agents entering a function call (a2 admission + a3 gather/D2H), then
-its retirement point (a4, a7).  By default the retirement is tc_retire — the previous cycle's transfers return their
-blocks and slots while this cycle's stream on, the asynchronous loop of P:645-648 (reading A8'); --retire sync drains
-every cycle with tc_sync instead (that number is also reported, as `per_cycle_drain`).
+its retirement point (a4, a7).  By default the retirement is tc_retire_lag(k) — the transfers enqueued before the
+k-th previous point return their blocks and slots while the last k cycles stream on, the asynchronous loop of
+P:645-648 (readings A8', A8''; k = the largest <= 4 the host buffer and free blocks carry, from the warm-up cycles);
+--retire sync drains every cycle with tc_sync instead (that number is also reported, as `per_cycle_drain`).
 
   python bench.py [--gpus N --steps K --warmup W] [--workload c2|c3|c4|c5] [--mode auto|direct|staged]
   python bench.py --impl reference ...     # the CPU oracle (oracle/), timed on the host cores
@@ -43,7 +44,7 @@ HBM_FALLBACK = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback (GB/s), 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=None)
@@ -59,6 +60,10 @@ def parse():
                          "draining this one's: the asynchronous loop of P:645-648); sync: tc_cycle + tc_sync "
                          "(drain every step); auto: each when the pool's host buffer and free blocks can carry a "
                          "second cycle in flight (judged from the warm-up cycles), else sync")
+    ap.add_argument("--retire-lag", type=int, default=0,
+                    help="retire-each loop: tc_retire_lag(lag) — retire what was enqueued before the lag-th previous "
+                         "point, so lag cycles stay in flight; 0 = auto: the largest lag <= 4 whose in-flight host "
+                         "slots and blocks fit (judged from the warm-up cycles)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--quick", action="store_true", help="skip host-link probe and device-tier microbench")
@@ -241,6 +246,7 @@ def run_ours(args):
     handles, sizes = {}, {}
 
     drains = [0]
+    lag = [1]
 
     def cycle(record=None, retire="sync"):
         """One scheduling cycle through the public API (tc_cycle: uploads then offloads), then its retirement point:
@@ -283,7 +289,7 @@ def run_ours(args):
                 if retire == "sync":
                     pool.sync()
                 else:
-                    pool.retire()
+                    pool.retire(lag[0])
         return nu, no
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
@@ -294,14 +300,17 @@ def run_ours(args):
     for _ in range(cfg.stall_cycles + 1):      # prime: get stalled agents to upload
         cycle()
     warm = [cycle() for _ in range(max(args.warmup, 3))]
-    if args.retire == "auto":                  # room for one more cycle in flight than a drained loop needs?
-        s = pool.stats()
-        up_max = max(u for u, _ in warm)
-        off_max = max(o for _, o in warm)
-        # retire-each keeps one more cycle of host slots (released by uploads) and of pending source blocks
-        # (offloads) unreturned than a drained loop does; 10 % margin over the warm-up's largest cycle
-        fits = s["host_free"] >= 2.2 * off_max and s["free"] >= 1.1 * (up_max + 2 * off_max)
-        args.retire = "each" if fits else "sync"
+    s = pool.stats()
+    up_max = max(u for u, _ in warm)
+    off_max = max(o for _, o in warm)
+
+    def fits(k):
+        # retire-each with lag k keeps k more cycles of host slots (released by uploads) and of pending source
+        # blocks (offloads) unreturned than a drained loop does; 10 % margin over the warm-up's largest cycle
+        return s["host_free"] >= 1.1 * (1 + k) * off_max and s["free"] >= 1.1 * (up_max + (1 + k) * off_max)
+    if args.retire == "auto":                  # room for at least one more cycle in flight than a drained loop?
+        args.retire = "each" if fits(1) else "sync"
+    lag[0] = args.retire_lag or max([k for k in range(1, 5) if fits(k)] or [1])
     # timed region: the kernels' own %globaltimer start/end only (timing mode 2: no extra events on the streams)
     pool.timing(2)
     pool.timing(2)                             # reset accumulators
@@ -495,7 +504,9 @@ def run_ours(args):
                    "l2": ("not flushed: every step streams ~2x the 126 MB L2 through blocks the previous steps did "
                           "not touch" if args.retire == "each" else
                           "flushed between steps (256 MiB write, outside the step events)"),
-                   "step": ("tc_cycle + tc_retire (retire the previous cycle's transfers, do not drain this one's); "
+                   "retire_lag": lag[0] if args.retire == "each" else None,
+                   "step": (f"tc_cycle + tc_retire_lag({lag[0]}) (retire the transfers enqueued before the "
+                            f"{lag[0]}-th previous point, do not drain the last {lag[0]} cycles'); "
                             "a cycle the host buffer / free blocks refuse is retried once after a tc_sync "
                             f"({drains[0]} of {n_steps} steps needed it); a tc_sync drains the last cycle inside the "
                             "timed region" if args.retire == "each" else

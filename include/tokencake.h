@@ -217,6 +217,12 @@ tc_status tc_sync(tc_pool *p);
    A serving loop calling tc_retire once per scheduling cycle returns last cycle's blocks and slots while this
    cycle's transfers stream on.  Ids stay a pure function of the call sequence.  A retirement point. */
 tc_status tc_retire(tc_pool *p);
+/* Retire with a lag (reading A8''; same passages): as tc_retire, but against the lag-th previous
+   retirement point — waits for and retires only the work enqueued before it, so the transfers of the last `lag`
+   scheduling cycles keep streaming while the caller enqueues the next one (a deeper asynchronous loop when one
+   cycle's uploads and offloads are unbalanced).  lag = 1 is tc_retire.  TC_E_INVAL for lag < 1 (no change, no new
+   retirement point).  Ids stay a pure function of the call sequence.  A retirement point. */
+tc_status tc_retire_lag(tc_pool *p, int32_t lag);
 
 /* ---- queries ------------------------------------------------------------------------------------------------- */
 tc_status tc_block_table(tc_pool *p, int32_t agent, int32_t *out, int64_t cap, int64_t *n_out); /* -1 = on host */

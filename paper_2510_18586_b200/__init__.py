@@ -29,7 +29,7 @@ SYMBOLS = [
     "tc_set_compute_stream", "tc_streams", "tc_set_xfer_mode", "tc_calibrate", "tc_set_launch_config", "tc_fill_kv", "tc_partition_reserve",
     "tc_agent_add", "tc_alloc", "tc_agent_free", "tc_offload", "tc_upload", "tc_offload_batch", "tc_upload_batch",
     "tc_cycle", "tc_reserve_begin", "tc_reserve_tick", "tc_reserve_cancel", "tc_reserve_info",
-    "tc_query", "tc_wait", "tc_stream_wait", "tc_sync", "tc_retire", "tc_block_table", "tc_block_table_dev", "tc_handle_info",
+    "tc_query", "tc_wait", "tc_stream_wait", "tc_sync", "tc_retire", "tc_retire_lag", "tc_block_table", "tc_block_table_dev", "tc_handle_info",
     "tc_handle_host", "tc_handle_read", "tc_stats", "tc_timing", "tc_timeline", "tc_trace", "tc_trace_read", "tc_strerror", "tc_last_error", "tc_gather_dev",
     "tc_scatter_dev",
     # decision layers (paper_2510_18586_b200/sched.py binds them)
@@ -137,6 +137,7 @@ def _load() -> ctypes.CDLL:
         "tc_stream_wait": (I32, [P, U64, VP]),
         "tc_sync": (I32, [P]),
         "tc_retire": (I32, [P]),
+        "tc_retire_lag": (I32, [P, I32]),
         "tc_block_table": (I32, [P, I32, PI32, I64, PI64]),
         "tc_block_table_dev": (I32, [P, ctypes.POINTER(PI32), PI64]),
         "tc_handle_info": (I32, [P, U64, PI32, PI64, PI32]),
@@ -315,9 +316,10 @@ class Pool:
     def sync(self):
         self._check(lib.tc_sync(self._h))
 
-    def retire(self):
-        """tc_retire: retire what was enqueued before the previous retire / sync point, without draining."""
-        self._check(lib.tc_retire(self._h))
+    def retire(self, lag: int = 1):
+        """tc_retire: retire what was enqueued before the previous retire / sync point, without draining;
+        lag > 1 (tc_retire_lag): before the lag-th previous point."""
+        self._check(lib.tc_retire(self._h) if lag == 1 else lib.tc_retire_lag(self._h, int(lag)))
 
     def cycle(self, up_handles, off_items):
         """One scheduling cycle (tc_cycle): uploads of `up_handles`, then offloads [(agent, ids), ...].

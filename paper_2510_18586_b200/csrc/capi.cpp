@@ -294,6 +294,14 @@ tc_status tc_retire(tc_pool *p) {
     TC_CATCH
 }
 
+tc_status tc_retire_lag(tc_pool *p, int32_t lag) {
+    TC_GUARD(p) {
+        TC_MUT("tc_retire_lag");
+        return P.retire(lag);
+    }
+    TC_CATCH
+}
+
 tc_status tc_sync(tc_pool *p) {
     TC_GUARD(p) {
         TC_MUT("tc_sync");

@@ -1298,14 +1298,17 @@ tc_status Pool::sync() {
 }
 
 // tc_retire (reading A8'): wait for and retire only the work enqueued before the previous retirement point — the
-// work of this epoch keeps running.
-tc_status Pool::retire() {
+// work of this epoch keeps running.  tc_retire_lag (A8''): the lag-th previous point, so the last lag epochs keep
+// running (lag 1 = tc_retire).
+tc_status Pool::retire(int32_t lag) {
+    if (lag < 1) return TC_E_INVAL;
+    const uint32_t upto = epoch_id + 1 > (uint32_t)lag ? epoch_id + 1 - (uint32_t)lag : 0;
     if (!meta_only) {
         if (cuda_dead) return TC_E_CUDA;
         for (int32_t e : ev_used)
-            if (ev_epoch[e] < epoch_id) TC_CUDA(cudaEventSynchronize(events[e]), "retire wait");
+            if (ev_epoch[e] < upto) TC_CUDA(cudaEventSynchronize(events[e]), "retire wait");
     }
-    retire_before(epoch_id);
+    retire_before(upto);
     return TC_OK;
 }
 

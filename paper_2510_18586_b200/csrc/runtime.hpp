@@ -134,7 +134,7 @@ struct Pool {
     std::vector<uint32_t> pending_epoch;     // retirement epoch of each pending entry (reading A8')
     uint32_t epoch_id = 0;                   // retirement points (tc_sync / tc_retire) so far
     std::vector<uint32_t> ev_epoch;          // per event index: the epoch it was last handed out in
-    tc_status retire();                      // tc_retire: retire what was enqueued before the previous point
+    tc_status retire(int32_t lag = 1);       // tc_retire(_lag): retire what was enqueued before the lag-th previous point
     void retire_before(uint32_t upto);
     std::vector<uint32_t> stamp;
     uint32_t epoch = 0;

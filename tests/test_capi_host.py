@@ -257,6 +257,29 @@ def test_fuzz_scripts_with_retire_match_oracle(seed, monkeypatch):
     replay_both(ops, N, S, ncls=2, P=P)
 
 
+@pytest.mark.parametrize("seed", range(16))
+def test_fuzz_scripts_with_retire_lag_match_oracle(seed, monkeypatch):
+    """Reading A8'' through the C ABI: tc_retire_lag with lags 1-3 and the refused 0, mixed with syncs, cycles,
+    gradual reservations and the peer tier; TC_CHECK on."""
+    monkeypatch.setenv("TC_CHECK", "1")
+    rng = np.random.default_rng(3000 + seed)
+    N, S, P = int(rng.choice([24, 64])), int(rng.choice([6, 16])), int(rng.choice([0, 4]))
+    ops = fuzz_script(900 + seed, n_ops=200, n_agents=3, n_classes=2, N=N, max_alloc=6, gradual=seed % 2 == 0,
+                      retire=True, lags=(0, 1, 2, 2, 3))
+    replay_both(ops, N, S, ncls=2, P=P)
+
+
+@pytest.mark.parametrize("name,lag", [("c2", 3), ("c3", 2)])
+def test_config_scripts_retire_lag_match_oracle(name, lag):
+    """bench.py's retire-each loop with a lag (tc_retire_lag), full size, metadata-only pool vs the oracle."""
+    cfg = CONFIGS[name]
+    ops = build_script(cfg, 8, combined=True)
+    n_setup = next(i for i, op in enumerate(ops) if op[0] == "cycle")
+    ops = ops[:n_setup] + [("retire", lag) if op[0] == "sync" else ("cycle_r",) + op[1:] if op[0] == "cycle" else op
+                           for op in ops[n_setup:]] + [("sync",)]
+    replay_both(ops, cfg.N, cfg.host_slots(), max_bpa=cfg.max_blocks_per_agent)
+
+
 @pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
 def test_config_scripts_retire_each_match_oracle(name):
     """bench.py's default loop at full size: tc_cycle + tc_retire per cycle, a refused cycle retried once after a

@@ -184,14 +184,18 @@ def sample_check(c: tcb.Pool, cfg, prov: np.ndarray, blocks: np.ndarray, seed: i
         assert np.array_equal(got[k], exp), (cfg.name, int(bl[k]), int(lk[k]))
 
 
-@pytest.mark.parametrize("name,world", [("c2", 1), ("c3", 1), ("c4", 1), ("c4", 8), ("c5", 8)])
-def test_full_size_config_parity(name, world):
+@pytest.mark.parametrize("name,world,lag", [("c2", 1, 1), ("c3", 1, 1), ("c4", 1, 1), ("c4", 8, 1), ("c5", 8, 1),
+                                            ("c2", 1, 4), ("c3", 1, 2)])
+def test_full_size_config_parity(name, world, lag):
+    """Full-size pools in bench.py's launch configuration: tc_cycle + tc_retire_lag(lag) per cycle (lag 1 =
+    tc_retire), byte parity on sampled chunks against the oracle's provenance, tables and counters exact."""
     cfg = CONFIGS[name]
     rank = world - 1 if world > 1 else 0
     S = cfg.host_slots()
     ops = build_script(cfg, 8, combined=True)          # tc_cycle + tc_retire per scheduling cycle, as bench.py times it
     n_setup = next(i for i, op in enumerate(ops) if op[0] == "cycle")
-    ops = ops[:n_setup] + [("retire",) if op[0] == "sync" else ("cycle_r",) + op[1:] if op[0] == "cycle" else op
+    rt = ("retire",) if lag == 1 else ("retire", lag)
+    ops = ops[:n_setup] + [rt if op[0] == "sync" else ("cycle_r",) + op[1:] if op[0] == "cycle" else op
                            for op in ops[n_setup:]] + [("sync",)]
     o = OraclePool(cfg.N, S, max_agents=1024, max_blocks_per_agent=cfg.max_blocks_per_agent,
                    store=ProvStore(cfg.N, S))
@@ -506,6 +510,19 @@ def test_retire_without_drain_bytes(mode):
                                         gradual=True, retire=True) if op[0] != "sync" or seed == 0]
         ops.append(("sync",))
         run_script(ops, L, H, D, N, S, mode, ncls=2, seed=seed + 11, T=T)
+
+
+@pytest.mark.parametrize("mode", ["auto", "staged"])
+def test_retire_lag_bytes(mode):
+    """Reading A8'' on the GPU: tc_retire_lag with lags 1-3 (and the refused 0) on scripts that retire often and sync
+    rarely; whole pool, host images, tables and counters equal the oracle after every sync."""
+    L, H, D, N, S, T = 4, 4, 128, 40, 24, 16
+    for seed in range(3):
+        ops = [op for op in fuzz_script(seed + 190, n_ops=150, n_agents=3, n_classes=2, N=N, max_alloc=6,
+                                        gradual=True, retire=True, lags=(0, 1, 2, 3, 3))
+               if op[0] != "sync" or seed == 0]
+        ops.append(("sync",))
+        run_script(ops, L, H, D, N, S, mode, ncls=2, seed=seed + 21, T=T)
 
 
 def test_retire_keeps_this_epochs_transfer_running():
