@@ -189,6 +189,21 @@ def hbm_peak():
         return HBM_FALLBACK, "B200_PROFILING.md fallback"
 
 
+def choose_retire(retire: str, retire_lag: int, host_free: int, free: int, up_max: int, off_max: int,
+                  max_lag: int = 4) -> tuple[str, int]:
+    """(retire mode, lag) for the timed loop, from the pool's free host slots / free blocks after the drained warm-up
+    cycles and the warm-up's largest upload / offload cycle (blocks).  Retire-each with lag k keeps k more cycles of
+    host slots (released by uploads) and of pending source blocks (offloads) unreturned than a drained loop does:
+    it fits when host_free >= 1.1 (1 + k) off_max and free >= 1.1 (up_max + (1 + k) off_max) (10 % margin).
+    auto -> each when lag 1 fits, else sync; lag 0 -> the largest k <= max_lag that fits (1 if none)."""
+    def fits(k):
+        return host_free >= 1.1 * (1 + k) * off_max and free >= 1.1 * (up_max + (1 + k) * off_max)
+    if retire == "auto":
+        retire = "each" if fits(1) else "sync"
+    lag = retire_lag or max([k for k in range(1, max_lag + 1) if fits(k)] or [1])
+    return retire, lag
+
+
 # ------------------------------------------------------------------------------------------------- our arm
 def run_ours(args):
     import torch
@@ -301,16 +316,8 @@ def run_ours(args):
         cycle()
     warm = [cycle() for _ in range(max(args.warmup, 3))]
     s = pool.stats()
-    up_max = max(u for u, _ in warm)
-    off_max = max(o for _, o in warm)
-
-    def fits(k):
-        # retire-each with lag k keeps k more cycles of host slots (released by uploads) and of pending source
-        # blocks (offloads) unreturned than a drained loop does; 10 % margin over the warm-up's largest cycle
-        return s["host_free"] >= 1.1 * (1 + k) * off_max and s["free"] >= 1.1 * (up_max + (1 + k) * off_max)
-    if args.retire == "auto":                  # room for at least one more cycle in flight than a drained loop?
-        args.retire = "each" if fits(1) else "sync"
-    lag[0] = args.retire_lag or max([k for k in range(1, 5) if fits(k)] or [1])
+    args.retire, lag[0] = choose_retire(args.retire, args.retire_lag, s["host_free"], s["free"],
+                                        max(u for u, _ in warm), max(o for _, o in warm))
     # timed region: the kernels' own %globaltimer start/end only (timing mode 2: no extra events on the streams)
     pool.timing(2)
     pool.timing(2)                             # reset accumulators
@@ -380,7 +387,7 @@ def run_ours(args):
     pool.timeline_arm(200000)
     if args.trace:
         pool.trace(100000)
-    n_diag = min(args.steps, 20)
+    n_diag = min(args.steps, int(os.environ.get("TC_DIAG_STEPS", 20)))
     # TC_DIAG_RETIRE=1: run the diagnostic cycles in the timed loop's retire-each form (one timeline over all of
     # them, for TC_DUMP_TIMELINE / tools/timeline_gaps.py) instead of drained
     diag_each = args.retire == "each" and os.environ.get("TC_DIAG_RETIRE") == "1"
