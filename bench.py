@@ -385,8 +385,7 @@ def run_ours(args):
     pool.timing(1)
     pool.timing(1)
     pool.timeline_arm(200000)
-    if args.trace:
-        pool.trace(100000)
+    pool.trace(100000)                         # per-call records: host enqueue cost of rows a2 / a5 (and --trace)
     n_diag = min(args.steps, int(os.environ.get("TC_DIAG_STEPS", 20)))
     # TC_DIAG_RETIRE=1: run the diagnostic cycles in the timed loop's retire-each form (one timeline over all of
     # them, for TC_DUMP_TIMELINE / tools/timeline_gaps.py) instead of drained
@@ -395,9 +394,11 @@ def run_ours(args):
         cycle(retire="retire" if diag_each else "sync")
     if diag_each:
         pool.sync()
+    trace_recs = pool.trace_read(100000)
+    pool.trace(0)
     if args.trace and rank == 0:
         with open(args.trace, "w") as f:
-            for r in pool.trace_read(100000):
+            for r in trace_recs:
                 f.write(json.dumps(r) + "\n")
     diag = pool.timing(0)
     tl_raw = pool.timeline(200000)
@@ -534,6 +535,7 @@ def run_ours(args):
             "how": "sum of the transfer kernels' device durations / the steps' device time: the fraction of the step "
                    "during which this path occupies SMs (the copy-engine DMAs use none); rank 0"},
         "timeline": tl_summary,
+        "host_enqueue": host_enqueue_summary(trace_recs, dev_total_ms / n_steps),
         "per_cycle_drain": other,
         "hostlink_peak": link,
         "roofline": roof,
@@ -591,6 +593,27 @@ def per_cycle_drain(torch, dev, cycle, ups, offs, B, n, flush):
         moved += (nu + no) * B
     return {"value": moved / (tot_ms * 1e-3) / 1e9 if tot_ms else None, "unit": "GB/s", "cycles": n,
             "how": "tc_cycle + tc_sync per cycle (drained), L2 flushed between cycles"}
+
+
+def host_enqueue_summary(recs, step_ms):
+    """Host cost of the integer rows of the path (a2 offload admission + host-slot pops + descriptors, a5 upload
+    allocation, the table rewrite, the launches / DMA enqueues) per tc_cycle call, from the per-call trace: entry of
+    the call -> the last of its batches enqueued.  Compared with the step's device time: the paper's pathology was
+    exactly here."""
+    cyc = {}
+    for r in recs:
+        c = cyc.setdefault(r["t_call_ns"], [0, 0])
+        c[0] = max(c[0], r["t_enqueued_ns"] - r["t_call_ns"])
+        c[1] += r["blocks"]
+    if not cyc:
+        return None
+    us = sorted(v[0] / 1e3 for v in cyc.values())
+    blocks = sum(v[1] for v in cyc.values())
+    return {"cycles": len(us), "p50_us": us[len(us) // 2], "p99_us": us[min(len(us) - 1, int(0.99 * len(us)))],
+            "mean_us": sum(us) / len(us), "ns_per_block": sum(us) * 1e3 / max(blocks, 1),
+            "share_of_step": (sum(us) / len(us)) / (step_ms * 1e3) if step_ms else None,
+            "how": "per tc_cycle: host ns from the call's entry to its last batch enqueued (tc_trace), diagnostic "
+                   "steps; share = mean / the timed region's ms_per_step"}
 
 
 def timeline_summary(spans):

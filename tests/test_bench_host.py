@@ -69,3 +69,14 @@ def test_choose_retire_lag():
     assert choose_retire("auto", 0, 10 ** 6, 3000, 1000, 1000) == ("sync", 1)
     assert choose_retire("each", 2, 0, 0, 1000, 1000) == ("each", 2)
     assert choose_retire("sync", 0, 10 ** 6, 10 ** 6, 10, 10) == ("sync", 4)
+
+
+def test_host_enqueue_summary():
+    """Per-cycle host enqueue cost from trace records: grouped by call, max enqueue lag, blocks summed."""
+    recs = [{"t_call_ns": 1000, "t_enqueued_ns": 41000, "blocks": 10},
+            {"t_call_ns": 1000, "t_enqueued_ns": 61000, "blocks": 30},
+            {"t_call_ns": 9000, "t_enqueued_ns": 29000, "blocks": 60}]
+    s = bench.host_enqueue_summary(recs, step_ms=1.0)
+    assert s["cycles"] == 2 and s["p50_us"] == 60.0 and abs(s["mean_us"] - 40.0) < 1e-9
+    assert abs(s["ns_per_block"] - 800.0) < 1e-9 and abs(s["share_of_step"] - 0.04) < 1e-12
+    assert bench.host_enqueue_summary([], 1.0) is None
