@@ -19,6 +19,7 @@ C5: G = 8, one rank's shard per GPU).  Prints ONE JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -97,6 +98,8 @@ class Clocks:
 
     def __init__(self, index: int):
         self.p = None
+        if os.environ.get("TC_BENCH_CLOCKS") == "0":     # experiments only: no sampler
+            return
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
                                        "--format=csv,noheader,nounits", "-lms", "200"],
@@ -323,6 +326,15 @@ def run_ours(args):
     pool.timing(2)                             # reset accumulators
     launches0 = pool.stats()["kernel_launches"]
     memcpy0 = pool.stats()["memcpy_calls"]
+    # the host loop is a serving engine's scheduler: no cyclic-GC pause inside it (a gen-2 collection over torch's
+    # heap takes milliseconds and lets the copy queues run dry); TC_BENCH_GC=1 keeps the collector on
+    gc_off = os.environ.get("TC_BENCH_GC") != "1"
+    trace_timed = os.environ.get("TC_TRACE_TIMED")          # experiments: per-call trace over the timed region
+    if trace_timed:
+        pool.trace(200000)
+    if gc_off:
+        gc.collect()
+        gc.disable()
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -377,6 +389,13 @@ def run_ours(args):
     if dist is not None:
         dist.barrier()
     t_wall = time.perf_counter() - t_wall0
+    if gc_off:
+        gc.enable()
+    if trace_timed:
+        with open(trace_timed, "w") as f:
+            for r in pool.trace_read(200000):
+                f.write(json.dumps(r) + "\n")
+        pool.trace(0)
     clk = clocks.stop()
     tim = pool.timing(0)
     launches = pool.stats()["kernel_launches"] - launches0
