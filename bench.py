@@ -562,7 +562,9 @@ def run_ours(args):
         "roofline_device": dev_bench,
         "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": (bytes_up + 16 * all_blocks) / n_steps,
                 "d2h_bytes_per_step": bytes_off / n_steps,
-                "how": "host wall clock around the public-API cycle (upload_batch, offload_batch, sync) per step"},
+                "how": "host wall clock around the public-API loop (tc_cycle from host id arrays — uploads, then "
+                       "offloads — and its retirement point, " + (f"tc_retire_lag({lag[0]}), a final tc_sync"
+                       if args.retire == "each" else "tc_sync") + "), KV bytes crossing the host link inside it"},
         "cpu_baseline": cpu,
         "clocks": clk,
         "wall_s": wall,
