@@ -192,6 +192,18 @@ def hbm_peak():
         return HBM_FALLBACK, "B200_PROFILING.md fallback"
 
 
+def per_gpu_summary(rows) -> dict:
+    """Per-rank throughput from rows [dev_ms, host_ms, bytes, blocks, wall_s] (one per rank): own bytes / own device
+    time, and the spread across ranks (flat per GPU = small spread)."""
+    gbs = [r[2] / (r[0] * 1e-3) / 1e9 if r[0] else 0.0 for r in rows]
+    bps = [r[3] / (r[0] * 1e-3) if r[0] else 0.0 for r in rows]
+    mean = sum(gbs) / len(gbs)
+    return {"gbs": gbs, "blocks_per_s": bps, "min_gbs": min(gbs), "max_gbs": max(gbs), "mean_gbs": mean,
+            "spread": (max(gbs) - min(gbs)) / mean if mean else None,
+            "how": "per rank: own KV bytes / own device time of the timed region (all_gather); value = all ranks' "
+                   "bytes / the max-over-ranks time"}
+
+
 def choose_retire(retire: str, retire_lag: int, host_free: int, free: int, up_max: int, off_max: int,
                   max_lag: int = 4) -> tuple[str, int]:
     """(retire mode, lag) for the timed loop, from the pool's free host slots / free blocks after the drained warm-up
@@ -431,10 +443,14 @@ def run_ours(args):
     my = torch.tensor([sum(dev_ms), sum(host_ms), bytes_up + bytes_off, blocks, t_wall], dtype=torch.float64,
                       device=dev if backend == "nccl" else "cpu")
     tot = my.clone()
+    rows = [my.cpu().tolist()]
     if dist is not None:
         mx = my.clone(); dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         sm = my.clone(); dist.all_reduce(sm, op=dist.ReduceOp.SUM)
         tot = torch.stack([mx[0], mx[1], sm[2], sm[3], mx[4]])
+        got = [torch.empty_like(my) for _ in range(world)]   # per-rank rows: flatness per GPU (the metric's "per GPU")
+        dist.all_gather(got, my)
+        rows = [g.cpu().tolist() for g in got]
     dev_total_ms, host_total_ms, all_bytes, all_blocks, wall = [float(x) for x in tot.cpu()]
 
     hbm, hbm_src = hbm_peak()
@@ -544,6 +560,7 @@ def run_ours(args):
                        peer_dev, "this GPU's own HBM" if peer_dev == local else "NVLink neighbour")) if args.peer
                    else "host"},
         "blocks_per_s": all_blocks / (dev_total_ms * 1e-3),
+        "per_gpu": per_gpu_summary(rows),
         "bytes_per_step": all_bytes / n_steps,
         "gpu_launches": int(launches),
         "memcpy_calls_per_step": (stats["memcpy_calls"] - memcpy0) / n_steps,

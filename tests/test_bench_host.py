@@ -80,3 +80,12 @@ def test_host_enqueue_summary():
     assert s["cycles"] == 2 and s["p50_us"] == 60.0 and abs(s["mean_us"] - 40.0) < 1e-9
     assert abs(s["ns_per_block"] - 800.0) < 1e-9 and abs(s["share_of_step"] - 0.04) < 1e-12
     assert bench.host_enqueue_summary([], 1.0) is None
+
+
+def test_per_gpu_summary():
+    """Per-rank GB/s = own bytes / own device ms; spread = (max - min) / mean."""
+    rows = [[10.0, 11.0, 1e9, 1000, 0.1], [20.0, 21.0, 1e9, 1000, 0.1]]
+    s = bench.per_gpu_summary(rows)
+    assert [round(x, 6) for x in s["gbs"]] == [100.0, 50.0]
+    assert [round(x) for x in s["blocks_per_s"]] == [100000, 50000]
+    assert abs(s["spread"] - 50.0 / 75.0) < 1e-12 and s["min_gbs"] == 50.0
