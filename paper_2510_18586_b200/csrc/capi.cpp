@@ -438,6 +438,7 @@ tc_status tc_timing(tc_pool *p, int32_t enable, tc_timing_t *out) {
             P.stamps_collect();
         }
         P.timing = P.meta_only ? 0 : enable;
+        if (P.timing) P.kts_ensure();                   // allocate now, not at the first timed launch
         if (out) {
             *out = P.tacc;
             P.tacc = tc_timing_t{};

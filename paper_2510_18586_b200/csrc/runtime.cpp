@@ -340,6 +340,16 @@ void Pool::stamps_collect() {
         const size_t used = kts_meta.size();
         std::vector<unsigned long long> buf(2 * used);
         if (cudaMemcpy(buf.data(), kts_dev, used * 16, cudaMemcpyDeviceToHost) == cudaSuccess) {
+            // TC_STAMP_DUMP=FILE (diagnostics): append "kind start_ns end_ns bytes" per launch
+            static const char *dump = std::getenv("TC_STAMP_DUMP");
+            if (dump) {
+                if (FILE *f = std::fopen(dump, "a")) {
+                    for (size_t i = 0; i < used; ++i)
+                        std::fprintf(f, "%d %llu %llu %lld\n", kts_meta[i].first, buf[2 * i], buf[2 * i + 1],
+                                     (long long)kts_meta[i].second);
+                    std::fclose(f);
+                }
+            }
             for (size_t i = 0; i < used; ++i) {
                 if (buf[2 * i + 1] < buf[2 * i]) continue;          // launch had no CTA with work
                 const int k = kts_meta[i].first;
@@ -356,18 +366,26 @@ void Pool::stamps_collect() {
 }
 
 // Kernel geometry for one launch; with tc_timing on, also a {start, end} %globaltimer slot for that launch.
+// The stamp buffer, allocated when timing is switched on (tc_timing), never inside a timed loop: a cudaMalloc there
+// can wait on the driver for tens of milliseconds.
+bool Pool::kts_ensure() {
+    if (kts_dev) return true;
+    if (cudaMalloc(&kts_dev, (size_t)kKts * 16) != cudaSuccess) { cudaGetLastError(); kts_dev = nullptr; return false; }
+    kts_init.assign(2 * kKts, 0);
+    for (int64_t i = 0; i < kKts; ++i) kts_init[2 * i] = ~0ull;
+    if (cudaMemcpy(kts_dev, kts_init.data(), (size_t)kKts * 16, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(kts_dev);
+        kts_dev = nullptr;
+        return false;
+    }
+    return true;
+}
+
 XferGeom Pool::geom(int32_t kind, int64_t bytes) {
     XferGeom g{N, C, 2 * L, nullptr};
     if (!timing || meta_only) return g;
-    if (!kts_dev) {
-        if (cudaMalloc(&kts_dev, (size_t)kKts * 16) != cudaSuccess) { cudaGetLastError(); kts_dev = nullptr; return g; }
-        kts_init.assign(2 * kKts, 0);
-        for (int64_t i = 0; i < kKts; ++i) kts_init[2 * i] = ~0ull;
-        if (cudaMemcpy(kts_dev, kts_init.data(), (size_t)kKts * 16, cudaMemcpyHostToDevice) != cudaSuccess) {
-            cudaGetLastError();
-            return g;
-        }
-    }
+    if (!kts_ensure()) return g;
     if ((int64_t)kts_meta.size() >= kKts) return g;      // more launches than slots before a sync: untimed
     g.ts = kts_dev + 2 * kts_meta.size();
     kts_meta.emplace_back(kind, bytes);

@@ -170,6 +170,7 @@ struct Pool {
     unsigned long long *kts_dev = nullptr;   // device {start, end} %globaltimer pairs, one per timed launch
     std::vector<unsigned long long> kts_init;
     std::vector<std::pair<int32_t, int64_t>> kts_meta;   // (kind, bytes) per used pair
+    bool kts_ensure();
     XferGeom geom(int32_t kind, int64_t bytes);
     // link-side transfer spans per direction, for the least-squares fit t = fixed + n * per_block
     // (tc_xfer_model_measure): sums of 1, n, t, n*n, n*t over the spans
