@@ -351,6 +351,7 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize(dev)
     dev_ms, host_ms, bytes_up, bytes_off, blocks, step_bytes = [], [], 0, 0, 0, []
+    host_step_s = []                           # retire-each: host time per step (enqueue + the retire wait)
     t_wall0 = time.perf_counter()
     if args.retire == "each":
         # the asynchronous loop: each step enqueues its cycle and retires the previous one's transfers
@@ -363,7 +364,9 @@ def run_ours(args):
             e.record(st)
         drains[0] = 0
         for k in range(args.steps):
+            th = time.perf_counter()
             nu, no = cycle(retire="retire")
+            host_step_s.append(time.perf_counter() - th)
             step_bytes.append((nu * B, no * B))
             bytes_up += nu * B
             bytes_off += no * B
@@ -572,6 +575,10 @@ def run_ours(args):
                    "during which this path occupies SMs (the copy-engine DMAs use none); rank 0"},
         "timeline": tl_summary,
         "host_enqueue": host_enqueue_summary(trace_recs, dev_total_ms / n_steps),
+        "host_steps": ({"p50_ms": statistics.median(host_step_s) * 1e3, "max_ms": max(host_step_s) * 1e3,
+                        "first_ms": host_step_s[0] * 1e3,
+                        "how": "retire-each: host wall time per step of the timed loop (tc_cycle + the retire wait); a "
+                               "max far above p50 is a host-side stall"} if host_step_s else None),
         "per_cycle_drain": other,
         "hostlink_peak": link,
         "roofline": roof,

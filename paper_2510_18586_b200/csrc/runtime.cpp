@@ -249,7 +249,8 @@ tc_status Pool::create(const tc_pool_desc &d) {
     if (auto_dir[0]) mode_d2h = auto_mode(0);
     if (auto_dir[1]) mode_h2d = auto_mode(1);
     auto_direct_bytes = env_int("TC_AUTO_DIRECT_KIB", 2048) * 1024ll;
-    for (int i = 0; i < 16; ++i) {
+    // completion events, created up front (a deep retire lag keeps dozens in flight; no driver call inside a loop)
+    for (int i = 0; i < 256; ++i) {
         cudaEvent_t e;
         TC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
         events.push_back(e);
