@@ -117,6 +117,9 @@ Pool::~Pool() {
     for (auto &sp : spans) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
     for (auto e : tev_free) cudaEventDestroy(e);
     if (ev_compute) cudaEventDestroy(ev_compute);
+    for (auto &d2 : half_free)
+        for (auto e : d2)
+            if (e) cudaEventDestroy(e);
     if (s_up) cudaStreamDestroy(s_up);
     if (s_up_k) cudaStreamDestroy(s_up_k);
     if (s_off_k) cudaStreamDestroy(s_off_k);
@@ -195,7 +198,10 @@ tc_status Pool::create(const tc_pool_desc &d) {
     piece_bytes = env_int("TC_PIECE_KIB", 256 * 1024) * 1024ll;
     head_bytes = env_int("TC_HEAD_KIB", 0) * 1024ll;
     use_batch_memcpy = env_int("TC_BATCH_MEMCPY", 1) != 0;
+    halves = env_int("TC_STAGING_HALVES", 1) != 0;
     TC_CUDA(cudaEventCreateWithFlags(&ev_compute, cudaEventDisableTiming), "event");
+    for (auto &d2 : half_free)
+        for (auto &e : d2) TC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     const int64_t kv_bytes = (int64_t)L * 2 * N * C;
     if (d.kv_dev) {
         if (reinterpret_cast<uintptr_t>(d.kv_dev) % 16) return TC_E_INVAL;
@@ -479,6 +485,20 @@ tc_status Pool::xfer_init(XferJob &j, bool gather, int32_t mode, const std::vect
     j.cut.push_back(j.n);
     j.npieces = (int64_t)j.cut.size() - 1;
     j.ev.assign(j.npieces, -1);
+    const int64_t half_bytes = (staging_bytes / 2) & ~255ll;  // half 1 starts 256-byte aligned (TMA needs 16)
+    if (j.npieces == 1 && halves && j.n * B <= half_bytes) {
+        // one piece that fits half the buffer: alternate halves across batches.  Gather: kernel on the aux stream,
+        // D2H on the main stream; upload: H2D on the aux stream, scatter (+ remap, completion) on the main stream.
+        // Each waits only for the previous use of its own half, so batch k's kernel overlaps batch k-1's DMA and
+        // the copy engine runs the direction's batches back to back.  The caller's GPU-side dependencies (offload
+        // / upload waits) are also placed on the aux stream (offload_waits / upload_waits).
+        j.half = half_next[dir];
+        half_next[dir] ^= 1;
+        j.stg = staging[dir] + (int64_t)j.half * half_bytes;
+        if (!gather) std::swap(j.s, j.sk);          // DMA stream = aux, kernel stream = main
+        TC_CUDA(cudaStreamWaitEvent(gather ? j.sk : j.s, half_free[dir][j.half], 0), "half reuse");
+        return TC_OK;
+    }
     if (j.npieces == 1) {                            // one piece: kernel and DMA in stream order, no cross-stream hop
         j.sk = j.s;
         return TC_OK;
@@ -527,7 +547,8 @@ tc_status Pool::calibrate(int64_t probe_bytes, tc_calibration_t *out) {
                 st = cuda_fail(cudaGetLastError(), "calibrate sync");
                 break;
             }
-            if (cudaEventRecord(e0, s_off) != cudaSuccess || cudaStreamWaitEvent(s_up, e0, 0) != cudaSuccess) {
+            if (cudaEventRecord(e0, s_off) != cudaSuccess || cudaStreamWaitEvent(s_up, e0, 0) != cudaSuccess ||
+                cudaStreamWaitEvent(s_up_k, e0, 0) != cudaSuccess || cudaStreamWaitEvent(s_off_k, e0, 0) != cudaSuccess) {
                 st = cuda_fail(cudaGetLastError(), "calibrate event");
                 break;
             }
@@ -757,23 +778,28 @@ tc_status Pool::xfer_phase_a(XferJob &j) {
 }
 
 tc_status Pool::xfer_phase_b(XferJob &j) {
-    if (j.n == 0 || j.mode != TC_XFER_STAGED || j.ring_reuse || j.gather) return TC_OK;
+    if (j.n == 0 || j.mode != TC_XFER_STAGED) return TC_OK;
     tc_status st;
-    for (int64_t p = 0; p < j.npieces; ++p) {
-        const int64_t a = j.cut[p], b = j.cut[p + 1];
-        char *base = xfer_base(j, p);
-        if (j.gather) {
-            TC_CUDA(cudaStreamWaitEvent(j.s, events[j.ev[p]], 0), "gather->D2H wait");
-            if ((st = xfer_copy(j, a, b, base)) != TC_OK) return st;
-        } else {
+    if (!j.ring_reuse && !j.gather) {
+        for (int64_t p = 0; p < j.npieces; ++p) {
+            const int64_t a = j.cut[p], b = j.cut[p + 1];
             if (j.sk != j.s) TC_CUDA(cudaStreamWaitEvent(j.sk, events[j.ev[p]], 0), "H2D->scatter wait");
-            if ((st = xfer_kernel(j, a, b, base)) != TC_OK) return st;
+            if ((st = xfer_kernel(j, a, b, xfer_base(j, p))) != TC_OK) return st;
+        }
+        if (j.half < 0 && j.sk != j.s) {              // the upload completes when its last scatter has
+            int32_t last;
+            if ((st = ev_rec(j.sk, &last)) != TC_OK) return st;
+            TC_CUDA(cudaStreamWaitEvent(j.s, events[last], 0), "scatter->upload join");
         }
     }
-    if (!j.gather && j.sk != j.s) {                   // the upload completes when its last scatter has
-        int32_t last;
-        if ((st = ev_rec(j.sk, &last)) != TC_OK) return st;
-        TC_CUDA(cudaStreamWaitEvent(j.s, events[last], 0), "scatter->upload join");
+    // staging fences for the halves mode: the stream on which this batch's last staging access completes (gather:
+    // the D2H on the main stream; halves upload: the scatter on the main stream; other uploads: joined into j.s)
+    const int dir = j.gather ? 0 : 1;
+    if (j.half >= 0) {
+        TC_CUDA(cudaEventRecord(half_free[dir][j.half], j.gather ? j.s : j.sk), "half free");
+    } else {                                           // a whole-buffer batch: both halves were (maybe) touched
+        TC_CUDA(cudaEventRecord(half_free[dir][0], j.s), "half free");
+        TC_CUDA(cudaEventRecord(half_free[dir][1], j.s), "half free");
     }
     return TC_OK;
 }
@@ -973,9 +999,13 @@ tc_status Pool::offload_waits(const OffPlan &P) {
         TC_CUDA(cudaEventRecord(ev_compute, s_compute), "compute event");
         TC_CUDA(cudaStreamWaitEvent(s_off, ev_compute, 0), "compute wait");
     }
+    if (s_compute) TC_CUDA(cudaStreamWaitEvent(s_off_k, ev_compute, 0), "compute wait");
     for (int32_t k = 0; k < P.na; ++k) {
         const int32_t ue = agents[P.ags[k]].up_event;
-        if (ue >= 0) TC_CUDA(cudaStreamWaitEvent(s_off, events[ue], 0), "upload->offload wait");
+        if (ue >= 0) {
+            TC_CUDA(cudaStreamWaitEvent(s_off, events[ue], 0), "upload->offload wait");
+            TC_CUDA(cudaStreamWaitEvent(s_off_k, events[ue], 0), "upload->offload wait");   // halves gathers
+        }
     }
     return TC_OK;
 }
@@ -1072,7 +1102,10 @@ tc_status Pool::plan_upload(UpPlan &P, int32_t nh, const tc_handle *hs, const in
 
 tc_status Pool::upload_waits(const UpPlan &P) {          // A13: the upload waits for each handle's offload
     for (int32_t k = 0; k < P.nh; ++k)
-        if (P.hr[k]->ev >= 0) TC_CUDA(cudaStreamWaitEvent(s_up, events[P.hr[k]->ev], 0), "offload->upload wait");
+        if (P.hr[k]->ev >= 0) {
+            TC_CUDA(cudaStreamWaitEvent(s_up, events[P.hr[k]->ev], 0), "offload->upload wait");
+            TC_CUDA(cudaStreamWaitEvent(s_up_k, events[P.hr[k]->ev], 0), "offload->upload wait");   // halves H2D
+        }
     return TC_OK;
 }
 

@@ -99,6 +99,11 @@ struct Pool {
     // streams / events
     cudaStream_t s_up = nullptr, s_off = nullptr, s_compute = nullptr;
     cudaStream_t s_up_k = nullptr, s_off_k = nullptr;   // staged mode: device-side kernels of each direction
+    // cross-batch double buffering of the staging buffer (single-piece batches that fit half of it): batch k of a
+    // direction uses half k % 2, so its kernel / DMA need not wait for batch k-1's DMA / kernel on the other half
+    bool halves = true;
+    int32_t half_next[2] = {0, 0};                      // per direction: the half the next batch uses
+    cudaEvent_t half_free[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [dir][half]: last use done
     int64_t piece_bytes = 256ll << 20;                  // staged pipeline: large pieces
     int64_t head_bytes = 0;                             // > 0: a small first (offload) / last (upload) piece
     bool use_batch_memcpy = true;
@@ -251,6 +256,7 @@ struct Pool {
     // two-phase transfer job (see runtime.cpp)
     struct XferJob {
         bool gather = false, ring_reuse = false;
+        int32_t half = -1;                   // >= 0: cross-batch double buffering on this staging half
         int32_t mode = TC_XFER_DIRECT;
         const std::vector<XferDesc> *desc = nullptr;
         const std::vector<int64_t> *slot_of = nullptr;
