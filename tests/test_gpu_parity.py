@@ -512,6 +512,19 @@ def test_retire_without_drain_bytes(mode):
         run_script(ops, L, H, D, N, S, mode, ncls=2, seed=seed + 11, T=T)
 
 
+@pytest.mark.parametrize("halves", ["0", "1"])
+def test_staging_halves_on_off_bytes(halves, monkeypatch):
+    """The staged path with and without the cross-batch staging halves (TC_STAGING_HALVES, read at pool creation):
+    a 5-block staging buffer mixes half-buffer batches (1-2 blocks, alternating halves), whole-buffer batches and ring
+    batches in one script; whole pool, host images, tables and counters equal the oracle after every sync."""
+    monkeypatch.setenv("TC_STAGING_HALVES", halves)
+    L, H, D, N, S, T = 4, 4, 128, 48, 32, 16
+    for seed in range(3):
+        ops = fuzz_script(seed + 290, n_ops=160, n_agents=4, n_classes=2, N=N, max_alloc=7, retire=True,
+                          lags=(1, 2, 3))
+        run_script(ops, L, H, D, N, S, "staged", ncls=2, seed=seed + 31, staging=5 * 2 * L * T * H * D * 2, T=T)
+
+
 @pytest.mark.parametrize("mode", ["auto", "staged"])
 def test_retire_lag_bytes(mode):
     """Reading A8'' on the GPU: tc_retire_lag with lags 1-3 (and the refused 0) on scripts that retire often and sync
