@@ -245,7 +245,7 @@ tc_status Pool::create(const tc_pool_desc &d) {
         cudaSetDevice(device);
         if (e != cudaSuccess) { cudaGetLastError(); peer.dev = nullptr; return TC_E_OOM; }
     }
-    staging_bytes = d.staging_bytes > 0 ? d.staging_bytes : (1ll << 30);
+    staging_bytes = d.staging_bytes > 0 ? d.staging_bytes : env_int("TC_STAGING_MIB", 1024) * (1ll << 20);
     if (staging_bytes < B) staging_bytes = B;
     // AUTO: the copy-engine staged path measured fastest for full cycles on B200 (profiles/r01_staged_ab.md).
     auto_dir[0] = mode_d2h == TC_XFER_AUTO;
