@@ -49,7 +49,25 @@ int main(int argc, char **argv) {
     CHECK(tc_stats(p, &s));
     printf("ok: 48 blocks offloaded and uploaded; first new id %d; free %lld alloc %lld host_free %lld\n",
            new_ids[0], (long long)s.free_blocks, (long long)s.alloc_blocks, (long long)s.host_free);
+
+    /* the asynchronous serving loop: each cycle offloads the agent and uploads it back, and retires with
+       a lag of 2 (reading A8''): the last two cycles' transfers keep streaming while the next one is enqueued */
+    for (int c = 0; c < 6; ++c) {
+        CHECK(tc_block_table(p, 1, table, 48, &n));
+        CHECK(tc_offload(p, 1, table, 48, &h));
+        CHECK(tc_upload(p, h, new_ids));
+        CHECK(tc_retire_lag(p, 2));
+    }
+    if (tc_retire_lag(p, 0) != TC_E_INVAL) { fprintf(stderr, "lag 0 not refused\n"); return 1; }
     CHECK(tc_sync(p));
+    CHECK(tc_stats(p, &s));
+    if (s.free_blocks + s.alloc_blocks != 1024 || s.alloc_blocks != 48 || s.host_free != 256) {
+        fprintf(stderr, "counters after the loop: free %lld alloc %lld host_free %lld\n", (long long)s.free_blocks,
+                (long long)s.alloc_blocks, (long long)s.host_free);
+        return 1;
+    }
+    printf("ok: 6 retire-lag cycles; free %lld alloc %lld host_free %lld\n", (long long)s.free_blocks,
+           (long long)s.alloc_blocks, (long long)s.host_free);
     tc_pool_destroy(p);
     return 0;
 }
