@@ -12,9 +12,12 @@ P:645-648 (readings A8', A8''; k = the largest <= 4 the host buffer and free blo
   python bench.py [--gpus N --steps K --warmup W] [--workload c2|c3|c4|c5] [--mode auto|direct|staged]
   python bench.py --impl reference ...     # the CPU oracle (oracle/), timed on the host cores
 
-Default workload: C2 (BASELINE.json configs[1], Qwen2.5-7B-shaped KV, Code-Writer-style 16 agents) on every rank —
-weak scaling over independent agent sets.  --workload c4 / c5 runs the head-sharded 32B / 70B configs (C4: G = N;
-C5: G = 8, one rank's shard per GPU).  Prints ONE JSON line on rank 0.
+--gpus N > 1 without a torchrun environment re-launches itself as N ranks (torch.distributed.run, 127.0.0.1), one
+process per GPU.  Default workload: at N = 1, C3 (BASELINE.json configs[2], Llama-3-8B-shaped KV, Deep-Research-style
+64 agents with Space-Scheduler partitions: the largest single-GPU config); at N > 1, C4 head-sharded with G = N (the
+north_star's KV-head partition: each GPU moves its own head shard of every block through its own host link; strong
+scaling).  --workload c2 / c3 run independent pools per rank (weak), --workload c5 one rank's G = 8 shard per GPU
+(weak) plus the 1-512 blocks-per-offload sweep.  Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
@@ -68,11 +71,45 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--quick", action="store_true", help="skip host-link probe and device-tier microbench")
+    ap.add_argument("--no-sweep", action="store_true", help="c5: skip the 1-512 blocks-per-offload sweep")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher / rendezvous / workload-plan check without a GPU: every rank joins the process group "
+                         "(gloo), rank 0 prints the plan line (n_gpus, head shards, per-rank rows, cpu_baseline)")
     return ap.parse_args()
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def launch_command(argv: list, gpus: int, port: int) -> list:
+    """The torchrun command bench.py re-executes itself with when --gpus N > 1 is given outside torchrun (the
+    driver's own N > 1 launch line, loopback rendezvous)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def self_launch(args, argv) -> int | None:
+    """--gpus N > 1 with no WORLD_SIZE in the environment: run N ranks through torchrun and return its exit code
+    (None = already inside a launcher, or a single GPU)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(launch_command(argv, args.gpus, free_port()), env=env)
 
 
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def default_workload(world: int) -> str:
+    """C3 on one GPU (the largest single-GPU config: 64 agents, Space-Scheduler quotas); the
+    head-sharded C4 (G = N) on N > 1 GPUs — the north_star's KV-head partition."""
+    return "c3" if world == 1 else "c4"
 
 
 def workload_for(args, world):
@@ -80,7 +117,7 @@ def workload_for(args, world):
     the whole 128 GiB pool sits on one GPU).  C5 is defined on 8 x B200 (BASELINE configs[4]): G = 8 always, and N < 8
     GPUs run N of its 8 rank shards (80 GiB each) — fixed work per GPU, weak scaling.  C1-C3: one whole pool per
     rank, independent agent sets (weak)."""
-    name = args.workload or "c2"
+    name = args.workload or default_workload(world)
     cfg = CONFIGS[name]
     if name == "c4":
         return cfg, world, ("strong" if world > 1 else "weak")
@@ -184,6 +221,77 @@ def hostlink_peak(torch, dev, nbytes=1 << 30, reps=10):
     return r
 
 
+def link_probe(torch, dev, dist, rank, world):
+    """(alone, concurrent) host-link peaks of this rank: alone = measured while every other rank waits at a barrier;
+    concurrent = all ranks measuring at once (the per-GPU denominator at N > 1).  At N = 1 they are one measurement."""
+    alone = None
+    for r in range(world):
+        if dist is not None:
+            dist.barrier()
+        if r == rank:
+            alone = hostlink_peak(torch, dev)
+    if world == 1:
+        return alone, alone
+    dist.barrier()
+    conc = hostlink_peak(torch, dev)
+    dist.barrier()
+    conc["how"] += ", all ranks concurrently"
+    alone["how"] += ", this rank alone (the others at a barrier)"
+    return alone, conc
+
+
+def offload_size_sweep(pool, cfg, B, sizes=None, reps=8):
+    """C5's "sweep 1-512 blocks per offload" (BASELINE configs[4]; the Fig. 11 micro-benchmark): two
+    sweep agents grown interleaved one block at a time (physically scattered ids); per size s and rep one tc_cycle
+    uploads s blocks of the agent offloaded last rep while it offloads s blocks of the other — both directions
+    concurrent — then the roles swap.  Per size: host call-return and completion (call -> both handles waited)
+    latency p50 / p99, and GB/s = 2 s B / completion p50."""
+    sizes = list(sizes or cfg.sweep or (1, 2, 4, 8, 16, 32, 64, 128, 256, 512))
+    smax = max(sizes)
+    pool.sync()
+    X, Y = 1022, 1023
+    for a in (X, Y):
+        pool.agent_add(a, 7)                 # background class: outside the Space-Scheduler quotas
+    for _ in range(smax):
+        pool.alloc(X, 1)
+        pool.alloc(Y, 1)
+    pool.sync()
+    rows = []
+    for sz in sizes:
+        h = pool.offload(Y, pool.block_table(Y)[:sz])
+        pool.wait(h)
+        pool.sync()
+        on, off_agent = X, Y                 # `on` is on the GPU and offloads; `off_agent` uploads handle h
+        call, done = [], []
+        for rep in range(reps + 2):
+            ids = pool.block_table(on)[:sz]
+            t0 = time.perf_counter()
+            _, hs = pool.cycle([h], [(on, ids)])
+            t1 = time.perf_counter()
+            pool.wait(h)
+            pool.wait(hs[0])
+            t2 = time.perf_counter()
+            pool.sync()
+            if rep >= 2:
+                call.append((t1 - t0) * 1e3)
+                done.append((t2 - t0) * 1e3)
+            h, on, off_agent = hs[0], off_agent, on
+        pool.upload(h)
+        pool.sync()
+        p50 = statistics.median(done)
+        rows.append({"blocks": sz, "bytes_per_direction": sz * B,
+                     "call_p50_ms": statistics.median(call), "call_p99_ms": float(np.percentile(call, 99)),
+                     "done_p50_ms": p50, "done_p99_ms": float(np.percentile(done, 99)),
+                     "gbs": 2 * sz * B / (p50 * 1e-3) / 1e9, "blocks_per_s": 2 * sz / (p50 * 1e-3)})
+    for a in (X, Y):
+        pool.agent_free(a)
+    pool.sync()
+    return {"rows": rows, "reps": reps, "block_shard_bytes": B,
+            "how": "per size s: tc_cycle(upload s blocks of one sweep agent, offload s blocks of the other) — both "
+                   "directions concurrent — from host arrays; call = host time of the tc_cycle call, done = call -> "
+                   "tc_wait of both handles; GB/s = 2 s B / done p50 (both directions)"}
+
+
 def hbm_peak():
     try:
         with open(PEAKS_PATH) as f:
@@ -193,15 +301,20 @@ def hbm_peak():
 
 
 def per_gpu_summary(rows) -> dict:
-    """Per-rank throughput from rows [dev_ms, host_ms, bytes, blocks, wall_s] (one per rank): own bytes / own device
-    time, and the spread across ranks (flat per GPU = small spread)."""
+    """Per-rank throughput from rows [dev_ms, host_ms, bytes, blocks, wall_s(, link bidir GB/s concurrent)] (one per
+    rank): own bytes / own device time, the spread across ranks (flat per GPU = small spread) and, when the rank's
+    concurrently measured link peak is in the row, own GB/s as a fraction of it."""
     gbs = [r[2] / (r[0] * 1e-3) / 1e9 if r[0] else 0.0 for r in rows]
     bps = [r[3] / (r[0] * 1e-3) if r[0] else 0.0 for r in rows]
     mean = sum(gbs) / len(gbs)
-    return {"gbs": gbs, "blocks_per_s": bps, "min_gbs": min(gbs), "max_gbs": max(gbs), "mean_gbs": mean,
-            "spread": (max(gbs) - min(gbs)) / mean if mean else None,
-            "how": "per rank: own KV bytes / own device time of the timed region (all_gather); value = all ranks' "
-                   "bytes / the max-over-ranks time"}
+    out = {"gbs": gbs, "blocks_per_s": bps, "min_gbs": min(gbs), "max_gbs": max(gbs), "mean_gbs": mean,
+           "spread": (max(gbs) - min(gbs)) / mean if mean else None,
+           "how": "per rank: own KV bytes / own device time of the timed region (all_gather); value = all ranks' "
+                  "bytes / the max-over-ranks time"}
+    if all(len(r) > 5 and r[5] for r in rows):
+        out["link_bidir_gbs"] = [r[5] for r in rows]
+        out["link_frac"] = [g / r[5] for g, r in zip(gbs, rows)]
+    return out
 
 
 def choose_retire(retire: str, retire_lag: int, host_free: int, free: int, up_max: int, off_max: int,
@@ -246,8 +359,13 @@ def run_ours(args):
                           "mixed": (tcb.XFER_DIRECT, tcb.XFER_STAGED),
                           "mixed_rev": (tcb.XFER_STAGED, tcb.XFER_DIRECT)}[args.mode]
     S = cfg.host_slots()
+    if args.gpus != world and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but {world} rank(s) in this launch; n_gpus reports {world}",
+              file=sys.stderr)
 
-    link = None if args.quick else hostlink_peak(torch, dev)
+    # host-link peaks: each rank alone (the others wait at a barrier), then all ranks at once — the concurrent one is
+    # the per-GPU denominator at N > 1 (shared PCIe switches / root complexes / host DRAM)
+    link_alone, link = (None, None) if args.quick else link_probe(torch, dev, dist, rank, world)
     peer_dev = ((local + 1) % torch.cuda.device_count()) if args.peer else -1
     pool = tcb.Pool(cfg.L, cfg.H, cfg.D, cfg.T, cfg.dtype, cfg.N, device=local, shard_rank=shard_rank, shard_world=G,
                     host_slots=S, max_agents=1024, max_blocks_per_agent=cfg.max_blocks_per_agent,
@@ -443,7 +561,13 @@ def run_ours(args):
         with open(os.environ["TC_DUMP_TIMELINE"], "w") as f:
             json.dump(tl_raw, f)
 
-    my = torch.tensor([sum(dev_ms), sum(host_ms), bytes_up + bytes_off, blocks, t_wall], dtype=torch.float64,
+    sweep = None
+    if cfg.name == "c5" and not args.no_sweep:      # BASELINE configs[4]: 1-512 blocks per offload (every rank)
+        if dist is not None:
+            dist.barrier()
+        sweep = offload_size_sweep(pool, cfg, B)
+    my = torch.tensor([sum(dev_ms), sum(host_ms), bytes_up + bytes_off, blocks, t_wall,
+                       link["bidir_gbs"] if link else 0.0], dtype=torch.float64,
                       device=dev if backend == "nccl" else "cpu")
     tot = my.clone()
     rows = [my.cpu().tolist()]
@@ -454,7 +578,7 @@ def run_ours(args):
         got = [torch.empty_like(my) for _ in range(world)]   # per-rank rows: flatness per GPU (the metric's "per GPU")
         dist.all_gather(got, my)
         rows = [g.cpu().tolist() for g in got]
-    dev_total_ms, host_total_ms, all_bytes, all_blocks, wall = [float(x) for x in tot.cpu()]
+    dev_total_ms, host_total_ms, all_bytes, all_blocks, wall = [float(x) for x in tot.cpu()[:5]]
 
     hbm, hbm_src = hbm_peak()
     dev_bench = None if args.quick else device_tier_bench(torch, pool, cfg, dev, hbm, hbm_src)
@@ -536,8 +660,8 @@ def run_ours(args):
                 link_roof[k + "_frac_of_unidir_peak"] = kern[k]["achieved_gbs"] / link[pk]
                 link_roof[k + "_frac_of_bidir_share"] = kern[k]["achieved_gbs"] / bi
     cpu = None
-    if not args.no_cpu_baseline and world == 1:
-        cpu = cpu_baseline(cfg, args.cpu_seconds)
+    if not args.no_cpu_baseline:               # rank 0, after the timed region (the other ranks wait at the barrier)
+        cpu = cpu_baseline(cfg, args.cpu_seconds, G)
     n_steps = args.steps
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": n_steps, "warmup": args.warmup,
@@ -581,6 +705,8 @@ def run_ours(args):
                                "max far above p50 is a host-side stall"} if host_step_s else None),
         "per_cycle_drain": other,
         "hostlink_peak": link,
+        "hostlink_peak_alone": link_alone,
+        "sweep": sweep,
         "roofline": roof,
         "roofline_link": link_roof,
         "roofline_device": dev_bench,
@@ -726,19 +852,34 @@ def device_tier_bench(torch, pool, cfg, dev, hbm, hbm_src):
 
 
 # ------------------------------------------------------------------------------------------------- CPU oracle
-def oracle_setup(cfg):
-    """Scaled copy of the workload for the host: same per-agent sizes and per-cycle counts, smaller N."""
+def oracle_scaled(cfg, G: int = 1):
+    """The bounded host sample of a workload for the oracle: the rank's block shard (G head shards, so the same
+    bytes per block as the GPU rank moves), a host-scaled pool of at most ~1.5 GB, at most 2 offloads + 2 uploads per
+    cycle and (per_cycle x (stall_cycles + 2)) agents whose log-normal sizes are clamped so they all fit."""
+    B = cfg.block_bytes(G)
+    N = int(min(4096, max(256, (3 << 29) // B)))
+    pc = min(cfg.per_cycle, 2)
+    n_agents = pc * (cfg.stall_cycles + 2)
+    hi = max(1, min(cfg.clamp[1], int(0.6 * N) // n_agents))
+    lo = min(cfg.clamp[0], hi)
+    return cfg.scaled(N=N, host_slots=int(N * 0.45), bg_fill=0.2, per_cycle=pc, n_agents=n_agents,
+                      med_blocks=min(cfg.med_blocks, hi), clamp=(lo, hi), G=G, churn=0.0)
+
+
+def oracle_setup(cfg, G: int = 1):
+    """The oracle (BytesStore: real pool and host-slot arrays) set up on oracle_scaled(cfg, G)."""
     from oracle import BytesStore, OraclePool
-    N = 1536 if cfg.block_bytes(1) <= (1 << 20) else 768
-    small = cfg.scaled(N=N, host_slots=int(N * 0.45), bg_fill=0.25)
-    C = small.chunk_bytes(1)
+    small = oracle_scaled(cfg, G)
+    N = small.N
+    C = small.chunk_bytes(G)
     pool0 = np.empty((small.L, 2, N, C), dtype=np.uint8)
-    pool0.reshape(-1)[:] = np.arange(pool0.size, dtype=np.uint64).astype(np.uint8)   # content irrelevant to timing
+    pool0.fill(0xA5)                                   # content is irrelevant to the timing of byte copies
     o = OraclePool(N, small.host_slots(), max_agents=1024, max_blocks_per_agent=small.max_blocks_per_agent,
                    store=BytesStore(pool0, small.host_slots()))
     from workloads.replay import Replayer
     ops, agents, _ = setup_ops(small)
-    Replayer(o).run(ops)
+    tr = Replayer(o).run(ops)
+    assert all(st == 0 for st, _ in tr), "host sample does not fit its pool"
     return small, o, agents
 
 
@@ -748,7 +889,7 @@ def oracle_cycles(small, o, agents, seconds=None, steps=None, warmup=0):
     r = Replayer(o)
     for a in agents:
         r.handles.setdefault(a, __import__("collections").deque())
-    B = small.block_bytes(1)
+    B = small.block_bytes(small.G)
 
     def one():
         nb = 0
@@ -776,12 +917,15 @@ def oracle_cycles(small, o, agents, seconds=None, steps=None, warmup=0):
     return blocks * B, sum(times), len(times)
 
 
-def cpu_baseline(cfg, seconds):
-    small, o, agents = oracle_setup(cfg)
+def cpu_baseline(cfg, seconds, G: int = 1):
+    small, o, agents = oracle_setup(cfg, G)
     nbytes, secs, cycles = oracle_cycles(small, o, agents, seconds=seconds)
     return {"value": nbytes / secs / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "sample": f"{cycles} cycles of {cfg.name} per-agent sizes on a host-scaled pool (N={small.N}, "
-                      f"{small.host_slots()} slots), NumPy BytesStore, single thread, {secs:.1f} s",
+            "sample": f"{cycles} cycles of {cfg.name} ({small.per_cycle} offloads + uploads per cycle, "
+                      f"{small.n_agents} agents, log-normal sizes clamped to [{small.clamp[0]}, {small.clamp[1]}] "
+                      f"blocks) on a host-scaled pool (N={small.N}, {small.host_slots()} slots, "
+                      f"{small.block_bytes(G)}-byte block shards, G={G}), NumPy BytesStore, single thread, "
+                      f"{secs:.1f} s",
             "host_cpu_count": os.cpu_count()}
 
 
@@ -789,26 +933,67 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    cfg, G, scaling = workload_for(args, 1)
-    small, o, agents = oracle_setup(cfg)
+    cfg, G, scaling = workload_for(args, world)
+    small, o, agents = oracle_setup(cfg, G)
     nbytes, secs, cycles = oracle_cycles(small, o, agents, steps=args.steps, warmup=args.warmup)
     value = nbytes / secs / 1e9
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3 / cycles, "higher_is_better": True,
         "scaling": scaling, "vs_baseline": None, "dtype": "u16 (bit copy of bf16 KV)", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: {cfg.title}", "host_scaled_n_blocks": small.N,
-                   "block_shard_bytes": small.block_bytes(1)},
+        "config": {"workload": f"{cfg.name}: {cfg.title}", "host_scaled_n_blocks": small.N, "head_shards": G,
+                   "block_shard_bytes": small.block_bytes(G)},
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{cycles} cycles on a host-scaled pool (N={small.N})"},
+                         "sample": f"{cycles} cycles of {cfg.name} ({small.per_cycle} offloads + uploads per cycle, "
+                                   f"{small.n_agents} agents, sizes clamped to [{small.clamp[0]}, {small.clamp[1]}]) "
+                                   f"on a host-scaled pool (N={small.N}, {small.block_bytes(G)}-byte block shards)"},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def run_dry(args):
+    """--dry-run: the N-rank plumbing without a GPU — rendezvous (gloo), the workload each rank would run, the
+    per-rank rows gathered to rank 0, the barrier / max / sum reductions, and rank 0's cpu_baseline."""
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    cfg, G, scaling = workload_for(args, world)
+    shard_rank = rank % G if G > 1 else 0
+    my = torch.tensor([1.0, 1.0, float(cfg.block_bytes(G)), 1.0, 0.0, 0.0], dtype=torch.float64)
+    rows = [my.tolist()]
+    shards = [shard_rank]
+    if world > 1:
+        dist.barrier()
+        got = [torch.empty_like(my) for _ in range(world)]
+        dist.all_gather(got, my)
+        rows = [g.tolist() for g in got]
+        sr = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(sr, torch.tensor([shard_rank], dtype=torch.int64))
+        shards = [int(x) for x in sr]
+    cpu = cpu_baseline(cfg, args.cpu_seconds, G) if rank == 0 and not args.no_cpu_baseline else None
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "metric": METRIC, "n_gpus": world, "scaling": scaling,
+                          "config": {"workload": f"{cfg.name}: {cfg.title}", "head_shards": G,
+                                     "shard_ranks": shards, "block_shard_bytes": cfg.block_bytes(G),
+                                     "parallelism": f"{world} ranks" + (f", head-sharded G={G}" if G > 1 else "")},
+                          "per_gpu": per_gpu_summary(rows), "cpu_baseline": cpu}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 if __name__ == "__main__":
     a = parse()
-    if a.impl == "reference":
+    rc = self_launch(a, sys.argv[1:])
+    if rc is not None:
+        sys.exit(rc)
+    if a.dry_run:
+        run_dry(a)
+    elif a.impl == "reference":
         run_reference(a)
     else:
         run_ours(a)

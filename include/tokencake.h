@@ -14,14 +14,17 @@
  *  - Ownership: the caller owns every array it passes; inputs are copied before return; outputs are written only on
  *    TC_OK.  Handles, pinned host slots, streams, events and (unless supplied externally) device memory are owned by
  *    the library and released by tc_pool_destroy.
- *  - Errors: strong guarantee — a non-OK status other than TC_E_CUDA leaves every piece of state unchanged.
- *    TC_E_NOHOST (offload refused) and TC_E_NOBLOCKS (upload "stalls"; the handle stays valid) are
- *    recoverable: retry after sync / free / re-quota.  TC_E_CUDA is sticky: the pool refuses further work and
- *    tc_last_error() says why.
+ *  - Errors: strong guarantee — a non-OK status other than TC_E_CUDA leaves every piece of state unchanged
+ *    ("pool unchanged").  TC_E_NOHOST (offload refused) and TC_E_NOBLOCKS (upload "stalls",
+ *    S:178; the handle stays valid) are recoverable: retry after sync / free / re-quota.  TC_E_OOM from a host
+ *    allocation is recoverable when it happens while a call is validated (nothing changed); the rare one after part
+ *    of a batch's GPU work was enqueued poisons the pool like TC_E_CUDA.  TC_E_CUDA is sticky: the pool refuses
+ *    further work and tc_last_error() says why.
  *  - Asynchrony: tc_offload / tc_upload return once the work is enqueued on the library's copy streams.  Logical
  *    state (block tables, counters) changes at call time; device/host bytes are valid after tc_wait / tc_stream_wait
- *    / tc_sync.  Freed device blocks and released host slots are reusable only after tc_sync (reading A8), so every
- *    id is a pure function of the call sequence, never of copy timing.
+ *    / tc_sync.  Freed device blocks and released host slots are reusable only after a retirement point — tc_sync
+ *    (reading A8), tc_retire (A8') or tc_retire_lag (A8''), each of which waits for exactly the transfers it
+ *    retires — so every id is a pure function of the call sequence, never of copy timing.
  *  - Layouts: KV pool [L][2][N][T][H/G][D] of 16-bit words (layer-major; chunk (block, layer, K|V) = C contiguous
  *    bytes, C = T*(H/G)*D*2; reading A3).  A host slot holds one block shard [L][2][C] = B = 2*L*C bytes (A4).
  *    Device block table int32[max_agents][max_blocks_per_agent], -1 = on host (A17).
@@ -51,7 +54,7 @@ typedef enum {
     TC_E_HANDLE = -4,    /* unknown handle, or already uploaded */
     TC_E_BUSY = -5,      /* agent_free while the agent has offloaded blocks / query: transfer still running */
     TC_E_CUDA = -6,      /* CUDA error (sticky); see tc_last_error */
-    TC_E_OOM = -7,       /* device or pinned-host allocation failed at create time */
+    TC_E_OOM = -7,       /* device / pinned-host allocation failed at create time, or a host allocation failed */
     TC_E_NODEV = -8      /* operation needs KV storage but the pool is metadata-only (device = -1) */
 } tc_status;
 
@@ -122,7 +125,10 @@ tc_status tc_pool_create_ex(const tc_pool_desc *d, tc_pool **out);
 void tc_pool_destroy(tc_pool *p);
 /* Device KV base pointer (layout above) and chunk bytes C. */
 tc_status tc_pool_kv(tc_pool *p, void **kv_dev, int64_t *chunk_bytes);
-/* Offloads wait (GPU-side) for work already queued on this stream, so an agent's last decode writes are captured. */
+/* The engine's compute (decode) stream.  Every later offload waits GPU-side for the work queued on it at the call, so
+   an agent's last decode writes are in the offloaded image (S:283 resume safety, P:645-648 cycle order), and
+   block-table pushes (tc_alloc) go on it.  NULL = none (pushes go on the offload stream).  The caller keeps the
+   stream alive while it is set. */
 tc_status tc_set_compute_stream(tc_pool *p, void *cuda_stream);
 /* The library's copy streams (upload = high priority), for event timing / dependencies by the caller. */
 tc_status tc_streams(tc_pool *p, void **upload_stream, void **offload_stream);
@@ -204,7 +210,11 @@ tc_status tc_reserve_tick(tc_pool *p);
 tc_status tc_reserve_cancel(tc_pool *p, tc_handle h);
 tc_status tc_reserve_info(tc_pool *p, tc_handle h, int64_t *reserved, int64_t *total);   /* readiness */
 
-/* TC_OK if the handle's last transfer has completed, TC_E_BUSY if not, TC_E_HANDLE if unknown. */
+/* Completion of a handle's latest transfer (a4 / a7; "after the transfer is complete", "never resumes
+   decode while any of its blocks are host-resident or in flight").  tc_query: TC_OK if it has completed, TC_E_BUSY
+   if not, TC_E_HANDLE if the handle is unknown (or forgotten, reading B3).  tc_wait: host-blocking wait.
+   tc_stream_wait: makes `cuda_stream` wait GPU-side (no host block) — the engine's decode of an uploaded agent is
+   enqueued after it and reads the scattered blocks and remapped table.  No state changes. */
 tc_status tc_query(tc_pool *p, tc_handle h);
 tc_status tc_wait(tc_pool *p, tc_handle h);                        /* host-blocking */
 tc_status tc_stream_wait(tc_pool *p, tc_handle h, void *cuda_stream); /* GPU-side dependency, no host block */
@@ -225,7 +235,13 @@ tc_status tc_retire(tc_pool *p);
 tc_status tc_retire_lag(tc_pool *p, int32_t lag);
 
 /* ---- queries ------------------------------------------------------------------------------------------------- */
+/* The agent's block table (host mirror): out[pos] = device block id, -1 = host-resident (the location flag of
+   P:649; reading A17); the remap of P:388 / P:646 is visible here at call time.  *n_out = the row length; at most
+   cap entries are written; out == NULL only queries the length (TC_E_INVAL if cap < the row length or the agent
+   is unknown). */
 tc_status tc_block_table(tc_pool *p, int32_t agent, int32_t *out, int64_t cap, int64_t *n_out); /* -1 = on host */
+/* The device copy of every table, int32[max_agents][row_stride], rewritten by the transfer kernels' epilogues in
+   stream order (the fused remap); library-owned unless supplied at create. */
 tc_status tc_block_table_dev(tc_pool *p, int32_t **dev_table, int64_t *row_stride);
 /* agent, block count, state (1 = offloaded, 2 = uploaded) of a live handle */
 tc_status tc_handle_info(tc_pool *p, tc_handle h, int32_t *agent, int64_t *n, int32_t *state);
@@ -235,6 +251,8 @@ tc_status tc_handle_host(tc_pool *p, tc_handle h, int64_t i, const void **host_p
    the caller's host buffer `dst` (blocking; waits for the handle's transfer).  TC_E_HANDLE if h is not offloaded,
    TC_E_INVAL for a bad i or dst, TC_E_NODEV on a metadata-only pool.  *tier (optional) = 0 host, 1 peer. */
 tc_status tc_handle_read(tc_pool *p, tc_handle h, int64_t i, void *dst, int32_t *tier);
+/* Allocator and transfer counters (S:113-115 conservation terms: free + alloc + pending (+ reserved) = N, host
+   free + used + released = S; per-class reserved / claimed of P:519-521).  Read-only. */
 tc_status tc_stats(tc_pool *p, tc_stats_t *s);
 /* Per-launch device timing (CUDA events recorded on the launching stream around every kernel / memcpy run).
    Spans complete at tc_sync, where their durations are accumulated.  Index (TC_NKINDS): 0 staged-mode device-side

@@ -34,6 +34,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     cmd = [nvcc(), "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
            "-Xcompiler", "-fPIC,-O3,-Wall", "-Xptxas", "-v" if verbose else "-O3", "-shared",
+           # the CUDA runtime as a shared library (the process's libcudart.so.12, e.g. torch's): the static one would
+           # embed the driver's whole entry-point table, including calls this build never makes
+           "-cudart", "shared", "-Xlinker", "-rpath," + os.path.join(os.path.dirname(os.path.dirname(nvcc())), "lib64"),
            "-I", os.path.join(ROOT, "include"),
            *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -395,7 +395,7 @@ tc_status tc_stats(tc_pool *p, tc_stats_t *s) {
         s->alloc_blocks = P.N - P.alloc.nfree - pend - P.n_reserved;
         s->reserved_blocks = P.n_reserved;
         s->host_slots = P.slots.count;
-        s->host_free = (int64_t)P.slots.free_list.size();
+        s->host_free = P.slots.nfree;
         s->host_released = (int64_t)P.slots.released.size();
         s->host_used = P.slots.count - s->host_free - s->host_released;
         s->chunk_bytes = P.C;
@@ -432,8 +432,7 @@ tc_status tc_timing(tc_pool *p, int32_t enable, tc_timing_t *out) {
         if (!P.meta_only && (!P.kts_meta.empty() || !P.spans.empty())) {   // collected lazily (runtime.cpp)
             for (cudaStream_t s : {P.s_up, P.s_off, P.s_up_k, P.s_off_k})
                 if (cudaStreamSynchronize(s) != cudaSuccess) return P.cuda_fail(cudaGetLastError(), "timing sync");
-            for (cudaStream_t f : P.foreign)
-                if (cudaStreamSynchronize(f) != cudaSuccess) return P.cuda_fail(cudaGetLastError(), "timing sync");
+            if (tc_status st = P.drain_foreign(); st != TC_OK) return st;
             P.spans_collect();
             P.stamps_collect();
         }

@@ -70,6 +70,54 @@ void BlockAllocator::set_free(int32_t b) {
     if ((b >> 6) < hint) hint = b >> 6;
 }
 
+// ------------------------------------------------------------------------------------------------ HostSlots
+void HostSlots::init(int64_t S) {
+    count = S;
+    const int64_t words = (S + 63) / 64;
+    bits.assign(words, ~0ull);
+    if (S % 64) bits[words - 1] = (1ull << (S % 64)) - 1;
+    nfree = S;
+}
+
+void HostSlots::choose(int64_t n, int64_t *out) const {
+    if (n <= 0) return;
+    int64_t start = 0, len = 0;
+    for (size_t w = 0; w < bits.size(); ++w) {
+        const uint64_t x = bits[w];
+        if (x == ~0ull) {                                  // a whole free word extends the run
+            if (len == 0) start = (int64_t)w * 64;
+            len += 64;
+            if (len >= n) break;
+            continue;
+        }
+        if (x == 0) {
+            len = 0;
+            continue;
+        }
+        for (int b = 0; b < 64; ++b) {
+            if ((x >> b) & 1) {
+                if (len == 0) start = (int64_t)w * 64 + b;
+                if (++len >= n) break;
+            } else {
+                len = 0;
+            }
+        }
+        if (len >= n) break;
+    }
+    if (len >= n) {
+        for (int64_t i = 0; i < n; ++i) out[i] = start + i;
+        return;
+    }
+    int64_t got = 0;                                       // fragmented: the lowest free slots
+    for (size_t w = 0; w < bits.size() && got < n; ++w)
+        for (uint64_t x = bits[w]; x && got < n; x &= x - 1) out[got++] = (int64_t)w * 64 + __builtin_ctzll(x);
+}
+
+void HostSlots::take(const int64_t *s, int64_t n) {
+    for (int64_t i = 0; i < n; ++i) bits[s[i] >> 6] &= ~(1ull << (s[i] & 63));
+    nfree -= n;
+}
+
 static int64_t steady_ns() {
     return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
         .count();
@@ -91,6 +139,15 @@ static void trace(const char *what) {
 }
 
 // ------------------------------------------------------------------------------------------------ Pool
+// A host allocation failed after part of a batch's GPU work was enqueued: the device may already be rewriting the
+// table / pool for a batch the host never committed, so the pool is poisoned like on a CUDA error (TC_E_OOM, then
+// TC_E_CUDA for every later call).  Allocation failures before the enqueue (plan_*) leave the pool unchanged.
+tc_status Pool::enqueue_oom() {
+    cuda_dead = true;
+    last_error = "host allocation failed while enqueueing a transfer (pool poisoned)";
+    return TC_E_OOM;
+}
+
 tc_status Pool::cuda_fail(cudaError_t e, const char *what) {
     cuda_dead = true;
     last_error = std::string(what) + ": " + cudaGetErrorString(e);
@@ -117,6 +174,10 @@ Pool::~Pool() {
     for (auto &sp : spans) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
     for (auto e : tev_free) cudaEventDestroy(e);
     if (ev_compute) cudaEventDestroy(ev_compute);
+    for (auto e : fev_live) cudaEventDestroy(e);
+    for (auto &ag : agents)
+        if (ag.push_ev) cudaEventDestroy(ag.push_ev);
+    for (auto e : fev_free) cudaEventDestroy(e);
     for (auto &d2 : half_free)
         for (auto e : d2)
             if (e) cudaEventDestroy(e);
@@ -158,10 +219,8 @@ tc_status Pool::create(const tc_pool_desc &d) {
     alloc.init(N, n_classes);
     agents.assign(max_agents, AgentRec{});
     stamp.assign(N, 0);
-    slots.count = S;
+    slots.init(S);
     slots.slot_bytes = B;
-    slots.free_list.resize(S);
-    for (int64_t i = 0; i < S; ++i) slots.free_list[i] = S - 1 - i;   // pop() yields 0, 1, 2, ...
     device = d.device;
     meta_only = d.device < 0;
     check = env_int("TC_CHECK", 0) != 0;
@@ -197,7 +256,6 @@ tc_status Pool::create(const tc_pool_desc &d) {
     TC_CUDA(cudaStreamCreateWithPriority(&s_off_k, cudaStreamNonBlocking, lo), "offload aux stream");
     piece_bytes = env_int("TC_PIECE_KIB", 256 * 1024) * 1024ll;
     head_bytes = env_int("TC_HEAD_KIB", 0) * 1024ll;
-    use_batch_memcpy = env_int("TC_BATCH_MEMCPY", 1) != 0;
     halves = env_int("TC_STAGING_HALVES", 1) != 0;
     TC_CUDA(cudaEventCreateWithFlags(&ev_compute, cudaEventDisableTiming), "event");
     for (auto &d2 : half_free)
@@ -246,7 +304,8 @@ tc_status Pool::create(const tc_pool_desc &d) {
         if (e != cudaSuccess) { cudaGetLastError(); peer.dev = nullptr; return TC_E_OOM; }
     }
     staging_bytes = d.staging_bytes > 0 ? d.staging_bytes : env_int("TC_STAGING_MIB", 1024) * (1ll << 20);
-    if (staging_bytes < B) staging_bytes = B;
+    // at least two blocks: a batch larger than the buffer alternates two halves of >= 1 block each (xfer_base)
+    if (staging_bytes < 2 * B) staging_bytes = 2 * B;
     // AUTO: the copy-engine staged path measured fastest for full cycles on B200 (profiles/r01_staged_ab.md).
     auto_dir[0] = mode_d2h == TC_XFER_AUTO;
     auto_dir[1] = mode_h2d == TC_XFER_AUTO;
@@ -418,7 +477,7 @@ char *Pool::ring_alloc(int64_t bytes, char **dev_ptr) {
         cudaStreamSynchronize(s_up);
         cudaStreamSynchronize(s_off);
         if (s_compute) cudaStreamSynchronize(s_compute);
-        for (cudaStream_t f : foreign) cudaStreamSynchronize(f);
+        drain_foreign();
         ring_head = 0;
         if (bytes > ring_cap) {
             cudaFreeHost(ring_host);
@@ -465,7 +524,7 @@ tc_status Pool::xfer_init(XferJob &j, bool gather, int32_t mode, const std::vect
     j.stg = staging[dir];
     j.sk = gather ? s_off_k : s_up_k;
     j.cut.clear();
-    const int64_t cap = staging_bytes / B;                       // blocks the staging buffer holds (>= 1)
+    const int64_t cap = staging_bytes / B;                       // blocks the staging buffer holds (>= 2)
     j.ring_reuse = j.n > cap;
     const int64_t edge = head_bytes > 0 ? std::max<int64_t>(1, head_bytes / B) : 0;   // head / tail blocks
     const int64_t big = std::max<int64_t>(1, piece_bytes / B);
@@ -521,16 +580,16 @@ tc_status Pool::calibrate(int64_t probe_bytes, tc_calibration_t *out) {
     if (probe_bytes <= 0 || !out) return TC_E_INVAL;
     for (cudaStream_t s : {s_up, s_off, s_up_k, s_off_k}) TC_CUDA(cudaStreamSynchronize(s), "calibrate drain");
     int64_t k = std::max<int64_t>(1, probe_bytes / B);
-    k = std::min<int64_t>({k, N / 2, (int64_t)slots.free_list.size() / 2});
+    k = std::min<int64_t>({k, N / 2, slots.nfree / 2});
     if (k < 1) return TC_E_NOHOST;
     std::vector<XferDesc> da(k), db(k);
-    std::vector<int64_t> sa(k), sb(k);
-    const size_t top = slots.free_list.size();
+    std::vector<int64_t> sa(k), sb(k), sfree(2 * k);
+    slots.choose(2 * k, sfree.data());             // free slots, used as scratch while the streams are drained
     for (int64_t i = 0; i < k; ++i) {              // A = blocks [0, k) (read), B = [k, 2k) (rewritten with itself)
         da[i] = XferDesc{(int32_t)i, -1, 0};
         db[i] = XferDesc{(int32_t)(k + i), -1, 0};
-        sa[i] = slots.free_list[top - 1 - i];
-        sb[i] = slots.free_list[top - 1 - k - i];
+        sa[i] = sfree[i];
+        sb[i] = sfree[k + i];
     }
     const bool saved_auto[2] = {auto_dir[0], auto_dir[1]};
     auto_dir[0] = auto_dir[1] = false;              // probe sizes exactly as given (no small-batch DIRECT)
@@ -586,9 +645,8 @@ tc_status Pool::calibrate(int64_t probe_bytes, tc_calibration_t *out) {
     return TC_OK;
 }
 
-// COPY mode: one strided DMA per block (2L rows of C bytes; pool row pitch N*C, slot rows packed), all blocks of the
-// batch in one cudaMemcpy3DBatchAsync call; the table epilogue is a small kernel in stream order (offload: first,
-// upload: after the data has landed).
+// COPY mode: one strided 2-D DMA per block (2L rows of C bytes; pool row pitch N*C, slot rows packed); the table
+// epilogue is a small kernel in stream order (offload: first, upload: after the data has landed).
 tc_status Pool::xfer_copy2d(XferJob &j) {
     const auto &slot_of = *j.slot_of;
     cudaEvent_t t0;
@@ -599,39 +657,18 @@ tc_status Pool::xfer_copy2d(XferJob &j) {
         n_launch += table_launches;
     }
     if ((st = span_begin(j.s, &t0)) != TC_OK) return st;
-    ops_.resize((size_t)j.n);
     for (int64_t i = 0; i < j.n; ++i) {
-        cudaMemcpy3DBatchOp &o = ops_[i];
-        std::memset(&o, 0, sizeof o);
         char *pool_p = kv + (int64_t)(*j.desc)[i].blk * C;
         char *host_p = host_ptr(slot_of[i]);
-        cudaMemcpy3DOperand dev{}, hst{};
-        dev.type = cudaMemcpyOperandTypePointer;
-        dev.op.ptr.ptr = pool_p;
-        dev.op.ptr.rowLength = (size_t)(N * C);
-        hst.type = cudaMemcpyOperandTypePointer;
-        hst.op.ptr.ptr = host_p;
-        hst.op.ptr.rowLength = (size_t)C;
-        o.src = j.gather ? dev : hst;
-        o.dst = j.gather ? hst : dev;
-        o.extent = make_cudaExtent((size_t)C, (size_t)(2 * L), 1);
-        o.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    }
-    size_t fail = 0;
-    cudaError_t e = use_batch_memcpy ? cudaMemcpy3DBatchAsync((size_t)j.n, ops_.data(), &fail, 0, j.s)
-                                     : cudaErrorNotSupported;
-    if (e != cudaSuccess) {                         // not available: one 2D copy per block
-        cudaGetLastError();
-        for (int64_t i = 0; i < j.n; ++i) {
-            const cudaMemcpy3DBatchOp &o = ops_[i];
-            TC_CUDA(cudaMemcpy2DAsync(o.dst.op.ptr.ptr, o.dst.op.ptr.rowLength, o.src.op.ptr.ptr,
-                                      o.src.op.ptr.rowLength, (size_t)C, (size_t)(2 * L),
-                                      j.gather ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, j.s),
-                    "2D memcpy");
-        }
+        if (j.gather)
+            TC_CUDA(cudaMemcpy2DAsync(host_p, (size_t)C, pool_p, (size_t)(N * C), (size_t)C, (size_t)(2 * L),
+                                      cudaMemcpyDeviceToHost, j.s), "2D memcpy");
+        else
+            TC_CUDA(cudaMemcpy2DAsync(pool_p, (size_t)(N * C), host_p, (size_t)C, (size_t)C, (size_t)(2 * L),
+                                      cudaMemcpyHostToDevice, j.s), "2D memcpy");
+        ++n_memcpy;
     }
     trace(j.gather ? "d2h" : "h2d");
-    ++n_memcpy;
     if ((st = span_end(j.s, j.gather ? 3 : 4, t0, j.n * B)) != TC_OK) return st;
     if (!j.gather) {
         TC_CUDA(launch_table(false, j.desc->data(), j.n, table_dev, j.s), "table kernel");
@@ -654,7 +691,8 @@ tc_status Pool::ev_rec(cudaStream_t st, int32_t *out) {
     return TC_OK;
 }
 
-// Copy-engine DMA of pieces [a, b) between the staging slot `base` and the host slots (one call per piece).
+// Copy-engine DMA of pieces [a, b) between the staging slot `base` and the host slots: one cudaMemcpyAsync per
+// contiguous run of host slots (one run for a batch whose slots HostSlots::choose found contiguous).
 tc_status Pool::xfer_copy(XferJob &j, int64_t a, int64_t b, char *base) {
     const bool to_host = j.gather;
     const auto &slot_of = *j.slot_of;
@@ -671,21 +709,6 @@ tc_status Pool::xfer_copy(XferJob &j, int64_t a, int64_t b, char *base) {
         cp_src.push_back(to_host ? (void *)dp : (void *)hp);
         cp_size.push_back((size_t)((k - i) * B));
         i = k;
-    }
-    if (cp_dst.size() > 1 && use_batch_memcpy) {
-        cudaMemcpyAttributes attr{};
-        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-        attr.flags = cudaMemcpyFlagDefault;
-        size_t attr_idx = 0, fail_idx = 0;
-        cudaError_t e = cudaMemcpyBatchAsync(cp_dst.data(), cp_src.data(), cp_size.data(), cp_dst.size(), &attr,
-                                             &attr_idx, 1, &fail_idx, j.s);
-        if (e == cudaSuccess) {
-            trace(to_host ? "d2h" : "h2d");
-            ++n_memcpy;
-            return span_end(j.s, to_host ? 3 : 4, t0, (b - a) * B);
-        }
-        cudaGetLastError();          // not supported here: fall back to one call per run, permanently
-        use_batch_memcpy = false;
     }
     for (size_t r = 0; r < cp_dst.size(); ++r) {
         TC_CUDA(cudaMemcpyAsync(cp_dst[r], cp_src[r], cp_size[r],
@@ -826,6 +849,13 @@ tc_status Pool::table_push(int32_t a, int64_t pos0, int64_t n) {
     TC_CUDA(cudaMemcpyAsync(table_dev + (int64_t)a * max_bpa + pos0, h, (size_t)n * 4, cudaMemcpyHostToDevice, s),
             "table push");
     ++n_memcpy;
+    // Without a compute stream the push runs on s_off, and a later offload's gather may run on the aux stream
+    // s_off_k (staging halves), which is not ordered after s_off: its table epilogue (-1) must not be overwritten
+    // by this push landing late.  offload_waits makes s_off_k wait on this event.
+    if (!s_compute) {
+        if (!ag.push_ev) TC_CUDA(cudaEventCreateWithFlags(&ag.push_ev, cudaEventDisableTiming), "push event");
+        TC_CUDA(cudaEventRecord(ag.push_ev, s), "push event");
+    }
     return TC_OK;
 }
 
@@ -856,6 +886,7 @@ tc_status Pool::alloc_blocks(int32_t a, int64_t k, int32_t *out) {
     const int64_t r = BlockAllocator::plan(ag.cls, k, alloc.nfree, alloc.reserved, alloc.claimed);
     if (r < 0) return TC_E_NOBLOCKS;
     const int64_t pos0 = (int64_t)ag.table.size();
+    ag.table.reserve((size_t)(pos0 + k));             // the only allocation; before any state changes
     alloc.take_lowest(k, out);
     alloc.claimed[ag.cls] += r;
     for (int64_t i = 0; i < k; ++i) {
@@ -892,7 +923,7 @@ tc_status Pool::plan_offload(OffPlan &P, int32_t na, const int32_t *ags, const i
     if (++epoch == 0) { std::fill(stamp.begin(), stamp.end(), 0); epoch = 1; }
     // per item, in order (B1: the first failing item's status): validity, then the tier — the whole offload to the
     // peer tier if its free list holds it, else to the CPU block buffer, else refused (reading C1)
-    const int64_t hf = (int64_t)slots.free_list.size(), pf = (int64_t)peer.free_list.size();
+    const int64_t hf = slots.nfree, pf = (int64_t)peer.free_list.size();
     int64_t ht = 0, pt = 0;
     std::vector<uint8_t> to_peer(na, 0);
     for (int32_t k = 0; k < na; ++k) {
@@ -921,11 +952,12 @@ tc_status Pool::plan_offload(OffPlan &P, int32_t na, const int32_t *ags, const i
     P.desc.resize(n);
     P.slot_of.resize(n);
     P.host_taken = P.peer_taken = 0;
-    if (!unbuffered) {                                  // LIFO pop order per tier (A16)
+    if (!unbuffered) {       // peer tier: LIFO pops (A16); host tier: one contiguous run for the batch (A16')
+        P.host_slots.resize(ht);
+        slots.choose(ht, P.host_slots.data());
         for (int32_t k = 0; k < na; ++k)
             for (int64_t i = off[k]; i < off[k + 1]; ++i)
-                P.slot_of[i] = to_peer[k] ? peer.free_list[pf - 1 - P.peer_taken++]
-                                          : slots.free_list[hf - 1 - P.host_taken++];
+                P.slot_of[i] = to_peer[k] ? peer.free_list[pf - 1 - P.peer_taken++] : P.host_slots[P.host_taken++];
     }
     if (unbuffered) {
         // Fig. 11 ablation: no CPU block buffer — pinned host memory is allocated for this offload now and freed
@@ -948,6 +980,30 @@ tc_status Pool::plan_offload(OffPlan &P, int32_t na, const int32_t *ags, const i
         for (int64_t i = off[k]; i < off[k + 1]; ++i)
             P.desc[i] = XferDesc{ids[i], ags[k] * max_bpa + alloc.own_pos[ids[i]], 0};
     split_tiers(P.desc, P.slot_of, P.ts);
+    // everything commit_offload stores is built (and its containers grown) here, before any state changes: a
+    // std::bad_alloc leaves the pool untouched (TC_E_OOM), and the commit itself cannot fail
+    P.pend.assign(na, {});
+    P.newh.clear();
+    P.newh.reserve(na);
+    for (int32_t k = 0; k < na; ++k) {
+        HandleRec hr;
+        hr.agent = ags[k];
+        hr.cls = agents[ags[k]].cls;
+        hr.state = kOffloaded;
+        const int64_t m = off[k + 1] - off[k];
+        hr.pos.reserve(m);
+        hr.slots.reserve(m);
+        P.pend[k].reserve(m);
+        for (int64_t i = off[k]; i < off[k + 1]; ++i) {
+            hr.pos.push_back(alloc.own_pos[ids[i]]);
+            hr.slots.push_back(P.slot_of[i]);
+            P.pend[k].push_back(ids[i]);
+        }
+        P.newh.emplace(next_handle + (tc_handle)k, std::move(hr));
+    }
+    pending_dev.reserve(pending_dev.size() + na);
+    pending_epoch.reserve(pending_epoch.size() + na);
+    handles.reserve(handles.size() + na);
     return TC_OK;
 }
 
@@ -1001,6 +1057,8 @@ tc_status Pool::offload_waits(const OffPlan &P) {
     }
     if (s_compute) TC_CUDA(cudaStreamWaitEvent(s_off_k, ev_compute, 0), "compute wait");
     for (int32_t k = 0; k < P.na; ++k) {
+        if (cudaEvent_t pe = agents[P.ags[k]].push_ev)
+            TC_CUDA(cudaStreamWaitEvent(s_off_k, pe, 0), "table push->offload wait");
         const int32_t ue = agents[P.ags[k]].up_event;
         if (ue >= 0) {
             TC_CUDA(cudaStreamWaitEvent(s_off, events[ue], 0), "upload->offload wait");
@@ -1011,39 +1069,31 @@ tc_status Pool::offload_waits(const OffPlan &P) {
 }
 
 // commit (a3 logical effects + a4 pending free); ev = the offload's completion event
-void Pool::commit_offload(const OffPlan &P, int32_t ev, tc_handle *out) {
+// (no allocation: plan_offload built the handle records and grew every container this touches)
+void Pool::commit_offload(OffPlan &P, int32_t ev, tc_handle *out) {
     const int64_t n = P.off[P.na];
     if (!unbuffered) {
-        slots.free_list.resize(slots.free_list.size() - P.host_taken);
+        slots.take(P.host_slots.data(), P.host_taken);
         peer.free_list.resize(peer.free_list.size() - P.peer_taken);
     }
     for (int32_t k = 0; k < P.na; ++k) {
         const int32_t a = P.ags[k];
         AgentRec &ag = agents[a];
-        HandleRec hr;
-        hr.agent = a;
-        hr.cls = ag.cls;
-        hr.state = kOffloaded;
-        hr.ev = ev;
-        std::vector<int32_t> pend;
         for (int64_t i = P.off[k]; i < P.off[k + 1]; ++i) {
             const int32_t b = P.ids[i];
-            const int32_t p = alloc.own_pos[b];
-            hr.pos.push_back(p);
-            hr.slots.push_back(P.slot_of[i]);
-            ag.table[p] = -1;                              // location flag -> host
+            ag.table[alloc.own_pos[b]] = -1;               // location flag -> host
             alloc.state[b] = kPending;                     // pending free until tc_sync
             alloc.own_agent[b] = -1;
             alloc.own_pos[b] = -1;
-            pend.push_back(b);
         }
-        pending_dev.emplace_back(ag.cls, std::move(pend));
+        pending_dev.emplace_back(ag.cls, std::move(P.pend[k]));
         pending_epoch.push_back(epoch_id);
         ++ag.live_offloads;
         const tc_handle h = next_handle++;
-        handles.emplace(h, std::move(hr));
+        P.newh.at(h).ev = ev;
         out[k] = h;
     }
+    handles.merge(P.newh);                                 // splices the prebuilt nodes (no rehash: reserved)
     if (!meta_only) bytes_d2h += n * B;
 }
 
@@ -1097,6 +1147,9 @@ tc_status Pool::plan_upload(UpPlan &P, int32_t nh, const tc_handle *hs, const in
         }
     }
     split_tiers(P.desc, P.slot_of, P.ts);
+    P.taken.resize(P.n_fresh);                    // commit_upload allocates nothing (strong guarantee on OOM)
+    slots.released.reserve(slots.released.size() + n);
+    slots.released_epoch.reserve(slots.released_epoch.size() + n);
     return TC_OK;
 }
 
@@ -1110,11 +1163,8 @@ tc_status Pool::upload_waits(const UpPlan &P) {          // A13: the upload wait
 }
 
 // commit (a5 allocation, a6 remap, a7 released slots); ev = the upload's completion event
-void Pool::commit_upload(const UpPlan &P, int32_t ev, int32_t *out_ids) {
-    if (P.n_fresh > 0) {
-        std::vector<int32_t> taken(P.n_fresh);
-        alloc.take_lowest(P.n_fresh, taken.data());   // identical to the planned ids (nothing changed since)
-    }
+void Pool::commit_upload(UpPlan &P, int32_t ev, int32_t *out_ids) {
+    if (P.n_fresh > 0) alloc.take_lowest(P.n_fresh, P.taken.data());   // == the planned ids (nothing changed since)
     for (int32_t k = 0; k < P.nh; ++k) {
         HandleRec &h = *P.hr[k];
         AgentRec &ag = agents[h.agent];
@@ -1152,7 +1202,7 @@ tc_status Pool::offload_batch(int32_t na, const int32_t *ags, const int64_t *off
     tc_status st = plan_offload(P, na, ags, off, ids);
     if (st != TC_OK) return st;
     int32_t ev = -1;
-    if (!meta_only) {
+    if (!meta_only) try {
         if ((st = offload_waits(P)) != TC_OK) return st;
         int32_t pj;
         if ((st = peer_launch(true, P.ts.pdesc, s_off, &pj)) != TC_OK) return st;
@@ -1161,6 +1211,8 @@ tc_status Pool::offload_batch(int32_t na, const int32_t *ags, const int64_t *off
             return st;
         if ((st = join(s_off, pj)) != TC_OK) return st;
         if ((st = ev_rec(s_off, &ev)) != TC_OK) return st;
+    } catch (const std::bad_alloc &) {
+        return enqueue_oom();
     }
     commit_offload(P, ev, out);
     trace_calls(1, ags, out, off, na, s_off);
@@ -1175,7 +1227,7 @@ tc_status Pool::upload_batch(int32_t nh, const tc_handle *hs, const int64_t *off
     tc_status st = plan_upload(P, nh, hs, off);
     if (st != TC_OK) return st;
     int32_t ev = -1;
-    if (!meta_only) {
+    if (!meta_only) try {
         if ((st = upload_waits(P)) != TC_OK) return st;
         int32_t pj;
         if ((st = peer_launch(false, P.ts.pdesc, s_up, &pj)) != TC_OK) return st;
@@ -1184,6 +1236,8 @@ tc_status Pool::upload_batch(int32_t nh, const tc_handle *hs, const int64_t *off
             return st;
         if ((st = join(s_up, pj)) != TC_OK) return st;
         if ((st = ev_rec(s_up, &ev)) != TC_OK) return st;
+    } catch (const std::bad_alloc &) {
+        return enqueue_oom();
     }
     commit_upload(P, ev, out_ids);
     trace_calls(2, nullptr, hs, off, nh, s_up);
@@ -1210,7 +1264,7 @@ tc_status Pool::cycle(int32_t nh, const tc_handle *hs, const int64_t *up_off, in
     if (na > 0 && (st = plan_offload(O, na, ags, off_off, ids)) != TC_OK) return st;
     trace("plans");
     int32_t ev_up = -1, ev_off = -1;
-    if (!meta_only) {
+    if (!meta_only) try {
         XferJob ju, jo;
         int32_t pu = -1, po = -1;                                     // peer-tier parts (NEXT-2)
         const bool pt = peer.count > 0;
@@ -1238,6 +1292,8 @@ tc_status Pool::cycle(int32_t nh, const tc_handle *hs, const int64_t *up_off, in
             if ((st = join(s_up, pu)) != TC_OK) return st;
             if ((st = ev_rec(s_up, &ev_up)) != TC_OK) return st;
         }
+    } catch (const std::bad_alloc &) {
+        return enqueue_oom();
     }
     if (nh > 0) commit_upload(U, ev_up, out_ids);
     if (na > 0) commit_offload(O, ev_off, out_h);
@@ -1340,7 +1396,7 @@ tc_status Pool::sync() {
         TC_CUDA(cudaStreamSynchronize(s_off), "sync offload stream");
         TC_CUDA(cudaStreamSynchronize(s_up_k), "sync upload aux stream");
         TC_CUDA(cudaStreamSynchronize(s_off_k), "sync offload aux stream");
-        for (cudaStream_t f : foreign) TC_CUDA(cudaStreamSynchronize(f), "sync caller stream");
+        if (tc_status st = drain_foreign(); st != TC_OK) return st;
         spans_collect();
         if ((int64_t)kts_meta.size() > kKts / 2) stamps_collect();
         ++sync_count;
@@ -1384,12 +1440,12 @@ void Pool::retire_before(uint32_t upto) {
     }
     pending_dev.resize(w);
     pending_epoch.resize(w);
-    // released slots back to their buffer; pushed in reverse so later pops replay ascending runs
+    // released slots back to their buffer
     for (size_t i = slots.released.size(); i-- > 0;) {
         if (slots.released_epoch[i] >= upto) continue;
         const int64_t x = slots.released[i];
         if (x < slots.count) {
-            slots.free_list.push_back(x);
+            slots.give(x);
         } else if (is_peer(x)) {                           // peer-tier slot: back to its own free list
             peer.free_list.push_back(x);
         } else {
@@ -1504,7 +1560,10 @@ void Pool::check_invariants(const char *after) const {
             for (int64_t s : kv.second.slots) (is_peer(s) ? peer_in_use : host_in_use) += 1;
         }
         for (int64_t s : slots.released) (is_peer(s) ? rel_peer : rel_host) += 1;
-        if ((int64_t)slots.free_list.size() + host_in_use + rel_host != slots.count) fail("host slot conservation");
+        if (slots.nfree + host_in_use + rel_host != slots.count) fail("host slot conservation");
+        int64_t nb = 0;
+        for (uint64_t x : slots.bits) nb += __builtin_popcountll(x);
+        if (nb != slots.nfree) fail("host free set != free count");
         if ((int64_t)peer.free_list.size() + peer_in_use + rel_peer != peer.count) fail("peer slot conservation");
     }
 }
@@ -1518,10 +1577,30 @@ tc_status Pool::device_tier(bool gather, const int32_t *ids, int64_t n, void *ex
         if (ids[i] < 0 || ids[i] >= N) return TC_E_INVAL;
         desc[i] = XferDesc{ids[i], -1, reinterpret_cast<uint64_t>(static_cast<char *>(ext) + i * B)};
     }
-    if (s && s != s_off && s != s_up && s != s_compute &&
-        std::find(foreign.begin(), foreign.end(), s) == foreign.end())
-        foreign.push_back(s);   // tc_sync also drains caller streams the device tier ran on
-    return enqueue_xfer(gather, TC_XFER_DIRECT, desc, {}, s ? s : s_off);
+    const bool foreign = s && s != s_off && s != s_up;
+    cudaEvent_t fe = nullptr;
+    if (foreign) {                  // tc_sync also waits for this launch: an event behind it, not the stream itself
+        if (fev_free.empty()) {
+            TC_CUDA(cudaEventCreateWithFlags(&fe, cudaEventDisableTiming), "caller-stream event");
+            fev_free.push_back(fe);
+        }
+        fev_live.reserve(fev_live.size() + 1);
+    }
+    tc_status st = enqueue_xfer(gather, TC_XFER_DIRECT, desc, {}, s ? s : s_off);
+    if (st != TC_OK || !foreign) return st;
+    fe = fev_free.back();
+    TC_CUDA(cudaEventRecord(fe, s), "caller-stream event");
+    fev_free.pop_back();
+    fev_live.push_back(fe);
+    return TC_OK;
+}
+
+// Waits for every device-tier launch made on a caller stream since the last drain.
+tc_status Pool::drain_foreign() {
+    for (cudaEvent_t e : fev_live) TC_CUDA(cudaEventSynchronize(e), "sync caller-stream work");
+    fev_free.insert(fev_free.end(), fev_live.begin(), fev_live.end());
+    fev_live.clear();
+    return TC_OK;
 }
 
 }  // namespace tc

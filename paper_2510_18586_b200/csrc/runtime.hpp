@@ -40,15 +40,28 @@ struct BlockAllocator {
     void set_free(int32_t b);
 };
 
-// CPU Block Buffering: one pinned slab cut into fixed block-shard slots + a LIFO free list.
+// CPU Block Buffering: one pinned slab cut into fixed block-shard slots + their free set.  Build choice
+// (reading A16'): a batch's slots are one contiguous run of the slab whenever one is free (lowest address
+// first), so the batch crosses the host link as one DMA per staging piece; otherwise the lowest free slots.  Slot
+// identity is outside the parity contract (A4); only counts are compared with the oracle's LIFO list.
 struct HostSlots {
     char *host = nullptr;            // host address of the slab
     char *dev = nullptr;             // device-visible (mapped) address of the same slab
     int64_t count = 0;
     int64_t slot_bytes = 0;
-    std::vector<int64_t> free_list;  // back() = next slot handed out
-    std::vector<int64_t> released;   // returned to free_list at a retirement point (tc_sync / tc_retire)
+    std::vector<uint64_t> bits;      // 1 = free
+    int64_t nfree = 0;
+    std::vector<int64_t> released;   // returned to the free set at a retirement point (tc_sync / tc_retire)
     std::vector<uint32_t> released_epoch;   // retirement epoch each released slot was created in
+
+    void init(int64_t S);
+    // n free slots: the lowest contiguous run of n if one exists, else the n lowest free slots.  No state change.
+    void choose(int64_t n, int64_t *out) const;
+    void take(const int64_t *s, int64_t n);
+    void give(int64_t s) {
+        bits[s >> 6] |= 1ull << (s & 63);
+        ++nfree;
+    }
 };
 
 // NEXT-2 peer tier: block-shard slots in a neighbouring GPU's HBM, ids S .. S+count-1, own LIFO free list.
@@ -65,6 +78,7 @@ struct AgentRec {
     std::vector<int32_t> table;      // host mirror; -1 = on host
     int32_t live_offloads = 0;       // handles in state OFFLOADED
     int32_t up_event = -1;           // event of the latest upload into this agent since the last sync
+    cudaEvent_t push_ev = nullptr;   // latest block-table push for this agent on s_off (no compute stream set)
 };
 
 struct HandleRec {
@@ -106,9 +120,11 @@ struct Pool {
     cudaEvent_t half_free[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [dir][half]: last use done
     int64_t piece_bytes = 256ll << 20;                  // staged pipeline: large pieces
     int64_t head_bytes = 0;                             // > 0: a small first (offload) / last (upload) piece
-    bool use_batch_memcpy = true;
     cudaEvent_t ev_compute = nullptr;
-    std::vector<cudaStream_t> foreign;       // caller streams used by the device tier
+    // caller streams the device tier ran on: an event recorded behind each such launch (the pool never holds the
+    // caller's stream handle, which the caller may destroy); tc_sync / tc_timing / ring wraps wait on these events
+    std::vector<cudaEvent_t> fev_live, fev_free;
+    tc_status drain_foreign();
     std::vector<cudaEvent_t> events;         // event pool
     std::vector<int32_t> ev_free, ev_used;
 
@@ -213,7 +229,11 @@ struct Pool {
         std::vector<XferDesc> desc;
         std::vector<int64_t> slot_of;
         int64_t host_taken = 0, peer_taken = 0;
+        std::vector<int64_t> host_slots;     // the batch's host-tier slots, in item order (HostSlots::choose)
         TierSplit ts;
+        // commit-time records built at plan time, so commit_offload allocates nothing (strong guarantee on OOM)
+        std::unordered_map<tc_handle, HandleRec> newh;
+        std::vector<std::vector<int32_t>> pend;
     };
     struct UpPlan {
         int32_t nh = 0;
@@ -226,16 +246,17 @@ struct Pool {
         std::vector<XferDesc> desc;
         std::vector<int64_t> slot_of;
         TierSplit ts;
+        std::vector<int32_t> taken;          // scratch for commit_upload's take_lowest (allocated at plan time)
     };
     void split_tiers(const std::vector<XferDesc> &desc, const std::vector<int64_t> &slot_of, TierSplit &ts) const;
     tc_status peer_launch(bool gather, const std::vector<XferDesc> &pd, cudaStream_t s, int32_t *join_ev);
     tc_status join(cudaStream_t s, int32_t ev);
     tc_status plan_offload(OffPlan &P, int32_t na, const int32_t *ags, const int64_t *off, const int32_t *ids);
     tc_status offload_waits(const OffPlan &P);
-    void commit_offload(const OffPlan &P, int32_t ev, tc_handle *out);
+    void commit_offload(OffPlan &P, int32_t ev, tc_handle *out);
     tc_status plan_upload(UpPlan &P, int32_t nh, const tc_handle *hs, const int64_t *off);
     tc_status upload_waits(const UpPlan &P);
-    void commit_upload(const UpPlan &P, int32_t ev, int32_t *out_ids);
+    void commit_upload(UpPlan &P, int32_t ev, int32_t *out_ids);
     tc_status query(tc_handle h, bool wait);
     tc_status stream_wait(tc_handle h, cudaStream_t s);
     tc_status sync();
@@ -249,6 +270,7 @@ struct Pool {
 
     // helpers
     tc_status cuda_fail(cudaError_t e, const char *what);
+    tc_status enqueue_oom();
     int32_t event_get();
     char *ring_alloc(int64_t bytes, char **dev_ptr);
     tc_status enqueue_xfer(bool gather, int32_t mode, const std::vector<XferDesc> &desc,
@@ -285,7 +307,6 @@ struct Pool {
     tc_status xfer_copy(XferJob &j, int64_t a, int64_t b, char *base);
     tc_status xfer_kernel(XferJob &j, int64_t a, int64_t b, char *base);
     tc_status xfer_copy2d(XferJob &j);
-    std::vector<cudaMemcpy3DBatchOp> ops_;   // scratch: COPY-mode DMA descriptors
     int32_t auto_mode(int dir) const;
     tc_status launch_descs(bool gather, int32_t kind, int path, const XferDesc *d, int64_t n, cudaStream_t s);
     std::vector<XferDesc> cd_;               // scratch: descriptors of the launch being built

@@ -89,3 +89,51 @@ def test_per_gpu_summary():
     assert [round(x, 6) for x in s["gbs"]] == [100.0, 50.0]
     assert [round(x) for x in s["blocks_per_s"]] == [100000, 50000]
     assert abs(s["spread"] - 50.0 / 75.0) < 1e-12 and s["min_gbs"] == 50.0
+
+
+@pytest.mark.parametrize("world,name,G,scaling", [(1, "c3", 1, "weak"), (2, "c4", 2, "strong"),
+                                                  (8, "c4", 8, "strong")])
+def test_default_workload_per_world(world, name, G, scaling):
+    """No --workload: C3 (largest single-GPU config) at N = 1, the head-sharded C4 with G = N at N > 1."""
+    cfg, g, sc = bench.workload_for(SimpleNamespace(workload=None), world)
+    assert (cfg.name, g, sc) == (name, G, scaling)
+
+
+def test_launch_command_is_loopback_torchrun():
+    cmd = bench.launch_command(["--gpus", "4", "--steps", "3"], 4, 29555)
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--nnodes=1" in cmd and "--master-port=29555" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-3:] == ["--gpus", "4", "--steps", "3"][-3:]
+
+
+def test_self_launch_two_ranks_dry_run():
+    """`bench.py --gpus 2` outside torchrun re-launches itself as two ranks (gloo in --dry-run): rank 0 prints one
+    line with n_gpus 2, the C4 head split G = 2 (shard ranks 0 and 1), two per-GPU rows and a cpu_baseline."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run",
+                          "--cpu-seconds", "1"], capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong"
+    assert d["config"]["head_shards"] == 2 and d["config"]["shard_ranks"] == [0, 1]
+    assert d["config"]["workload"].startswith("c4")
+    assert len(d["per_gpu"]["gbs"]) == 2
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
+
+
+@pytest.mark.parametrize("name,G", [("c2", 1), ("c3", 1), ("c4", 1), ("c4", 2), ("c4", 8), ("c5", 8)])
+def test_oracle_host_sample_fits(name, G):
+    """The cpu_baseline / reference-arm host sample of every config fits its scaled pool (no refused op), keeps the
+    rank's block-shard size and stays within ~1.5 GB of pool bytes."""
+    from workloads.configs import CONFIGS
+    cfg = CONFIGS[name]
+    small = bench.oracle_scaled(cfg, G)
+    assert small.block_bytes(G) == cfg.block_bytes(G)
+    assert small.N * small.block_bytes(G) <= (3 << 29) + small.block_bytes(G) or small.N == 256
+    from workloads.scripts import agent_sizes
+    import numpy as np
+    sizes = agent_sizes(small, np.random.default_rng(small.seed))
+    assert sum(sizes) <= 0.6 * small.N + len(sizes)
