@@ -168,6 +168,57 @@ class SetModel:
         self.clm[c] = max(0, self.clm[c] - len(mine))
         self.tab[a] = []
 
+    # ---- one cycle's batches (readings B1, B5).  Written as validate-then-apply: every item is checked in
+    # order against the state the earlier items would leave (ownership, distinct ids, host / peer room, block room
+    # under the partition rule) without touching anything, and only a fully valid batch is applied item by item.
+    def _check_offloads(self, items):
+        gone = set()
+        room_p, room_h = len(self.pstack), len(self.stack)
+        for a, ids in items:
+            if not ids or len(set(ids)) < len(ids) or any(b in gone or self.own.get(b, (None,))[0] != a for b in ids):
+                raise Fail(INVAL)
+            if room_p >= len(ids):
+                room_p -= len(ids)
+            elif room_h >= len(ids):
+                room_h -= len(ids)
+            else:
+                raise Fail(NOHOST)
+            gone.update(ids)
+
+    def _check_uploads(self, hs):
+        seen = set()
+        nfree, clm = len(self.free), list(self.clm)
+        for h in hs:
+            if h not in self.live or h in seen:
+                raise Fail(HANDLE)
+            seen.add(h)
+            c, pos = self.live[h][1], self.live[h][2]
+            n = len(pos) - len(self.rsv.get(h, []))
+            if n <= 0:
+                continue
+            unc = [max(0, r - k) for r, k in zip(self.res, clm)]
+            r = min(unc[c], n)
+            if n > nfree or n - r > max(0, nfree - sum(unc)):
+                raise Fail(NOBLOCKS)
+            clm[c] += r
+            nfree -= n
+
+    def offload_batch(self, items):
+        self._check_offloads(items)
+        return [self.offload(a, ids) for a, ids in items]
+
+    def upload_batch(self, hs):
+        self._check_uploads(hs)
+        return [self.upload(h) for h in hs]
+
+    def cycle(self, hs, items):
+        # uploads' status first; the offloads are checked against the pre-cycle owners, so a block this cycle's
+        # uploads allocate (free or reserved now) is never an on-GPU block of the agent: INVAL (B5)
+        self._check_uploads(hs)
+        self._check_offloads(items)
+        news = [self.upload(h) for h in hs]
+        return news, [self.offload(a, ids) for a, ids in items]
+
     def counts(self):
         npend = sum(len(i) for _, i, _ in self.pend)
         return len(self.free), len(self.own), npend

@@ -26,6 +26,12 @@ ALPHABET_R = ALPHABET + [("reserve_begin", 2), ("tick",)]
 ALPHABET_RT = ALPHABET + [("retire",)]
 # reading A8'': retire against the lag-th previous point (lag 2), and the refused lag 0
 ALPHABET_RL = ALPHABET + [("retire",), ("retire", 2), ("retire", 0)]
+# readings B1 / B5: one cycle's batches — two agents' offloads, an overlapping pair (INVAL at item 2),
+# all live uploads, a duplicate upload (HANDLE), uploads-then-offloads cycles, and a cycle whose offload names the
+# lowest free block for the uploaded agent (the block its own upload takes: B5)
+ALPHABET_B = ALPHABET + [("offload_batch", ((A, "all"), (B, "all"))), ("offload_batch", ((A, "first"), (A, "all"))),
+                         ("upload_batch", "all"), ("upload_batch", "dup"), ("cycle", (B, "all")),
+                         ("cycle", (A, "first")), ("cycle_b5",)]
 
 
 def sel_ids(table, sel):
@@ -33,9 +39,40 @@ def sel_ids(table, sel):
     return on if sel == "all" else on[:1]
 
 
+def live_handles(live):
+    return sorted(live)
+
+
+def batch_args(op, tab, live, free, owner):
+    """The concrete arguments of a batch op, from the pre-op state (identical on both sides): tab(a) = agent a's
+    table, live = live handles ascending, free = free block ids ascending, owner(h) = the agent of handle h."""
+    k = op[0]
+    if k == "offload_batch":
+        return [(a, sel_ids(tab(a), sel)) for a, sel in op[1]]
+    if k == "upload_batch":
+        if not live:
+            return [0]
+        return live if op[1] == "all" else [live[0], live[0]]
+    if k == "cycle":
+        a, sel = op[1]
+        return live[:1], [(a, sel_ids(tab(a), sel))]
+    if k == "cycle_b5":
+        return live[:1], [(owner(live[0]) if live else A, free[:1] or [0])]
+    raise AssertionError(op)
+
+
 def run_oracle(p: OraclePool, op):
     try:
         k = op[0]
+        if k in ("offload_batch", "upload_batch", "cycle", "cycle_b5"):
+            live = live_handles(h for h, x in p.handles.items() if x.state == OFFLOADED)
+            free = [b for b in range(len(p.blk_state)) if p.blk_state[b] == 0]
+            args = batch_args(op, p.block_table, live, free, lambda h: p.handles[h].agent)
+            if k == "offload_batch":
+                return 0, p.offload_batch(args)
+            if k == "upload_batch":
+                return 0, p.upload_batch(args)
+            return 0, p.cycle(*args)
         if k == "alloc":
             return 0, p.alloc(op[1], op[2])
         if k == "offload":
@@ -65,6 +102,14 @@ def run_oracle(p: OraclePool, op):
 def run_model(m: SetModel, op):
     try:
         k = op[0]
+        if k in ("offload_batch", "upload_batch", "cycle", "cycle_b5"):
+            live = live_handles(m.live)
+            args = batch_args(op, lambda a: m.tab[a], live, sorted(m.free), lambda h: m.live[h][0])
+            if k == "offload_batch":
+                return 0, m.offload_batch(args)
+            if k == "upload_batch":
+                return 0, m.upload_batch(args)
+            return 0, m.cycle(*args)
         if k == "alloc":
             return 0, m.alloc(op[1], op[2])
         if k == "offload":
@@ -124,7 +169,7 @@ def key(p: OraclePool, m: SetModel):
             tuple(sorted((h, tuple(v)) for h, v in m.rsv.items())))
 
 
-def explore(N, S, depth, alphabet=ALPHABET, P=0):
+def explore(N, S, depth, alphabet=ALPHABET, P=0, seen_status=None):
     pool0 = content.pool_bytes(9, 1, N, 1, 1, 8)          # C = 16 bytes per chunk
     p = OraclePool(N, S, n_classes=2, store=BytesStore(pool0, S + P), n_peer_slots=P)
     m = SetModel(N, S, P=P)
@@ -147,6 +192,8 @@ def explore(N, S, depth, alphabet=ALPHABET, P=0):
             nodes[0] += 1
             where = path + [op]
             assert ro == rm, (where, ro, rm)
+            if seen_status is not None:
+                seen_status.add((op[0], ro[0]))
             compare(p2, m2, pool0, where)
             dfs(p2, m2, d - 1, where)
 
@@ -221,4 +268,26 @@ def test_bruteforce_retire_lag(N, S, depth):
     """Every sequence over the 15-op alphabet plus retire with lag 1, 2 and the refused 0 (reading A8'': retire only
     what was enqueued before the lag-th previous retirement point) against the set model with its own epochs."""
     nodes, states = explore(N, S, depth, alphabet=ALPHABET_RL)
+    assert nodes > 1000 and states > 100
+
+
+@pytest.mark.parametrize("N,S,depth", [(4, 3, 5), (5, 2, 5), (6, 4, 4)])
+def test_bruteforce_batches_and_cycles(N, S, depth):
+    """Every sequence over the 15-op alphabet plus seven batch / cycle ops (readings B1, B5: all-or-nothing, first
+    failing item's status, uploads before offloads, no offload of a block the cycle's own uploads allocate) against
+    the set model's validate-then-apply batches; payload, tables, counters, slot lists and handles after every op."""
+    seen = set()
+    nodes, states = explore(N, S, depth, alphabet=ALPHABET_B, seen_status=seen)
+    assert nodes > 1000 and states > 100
+    # the batch paths' outcomes all occur: success, INVAL (overlap / B5 / empty), HANDLE (duplicate), NOBLOCKS / NOHOST
+    for st in ((("offload_batch", 0), ("offload_batch", -1), ("upload_batch", 0), ("upload_batch", -4),
+                ("cycle", 0), ("cycle", -1), ("cycle_b5", -1))):
+        assert st in seen, st
+    assert {("offload_batch", -3), ("cycle", -3), ("upload_batch", -2), ("cycle", -2)} & seen
+
+
+@pytest.mark.parametrize("N,S,P,depth", [(5, 2, 2, 5)])
+def test_bruteforce_batches_peer_tier(N, S, P, depth):
+    """The batch / cycle alphabet with a peer tier: per-item tier choice inside a batch (NEXT-2, reading C1)."""
+    nodes, states = explore(N, S, depth, alphabet=ALPHABET_B, P=P)
     assert nodes > 1000 and states > 100

@@ -61,7 +61,10 @@ def test_invariants_and_round_trip_on_fuzz(seed):
         hbefore = p.next_handle
         live_before = {h for h, x in p.handles.items() if x.state == OFFLOADED}
         pool_before = p.store.pool.copy()
+        state_before = whole_state(p)
         st, out = r.step(op)
+        if st != 0:                                    # strong guarantee: a refused op changes nothing at all
+            assert states_equal(state_before, whole_state(p)), op
         if st == 0 and op[0] in ("offload", "offload_batch", "cycle"):
             for h in range(hbefore, p.next_handle):
                 hd = p.handles[h]
@@ -89,6 +92,27 @@ def test_invariants_and_round_trip_on_fuzz(seed):
         if sound and op[0] != "reserve":
             assert now_sound, op                       # selects preserve soundness (reading A9)
         sound = now_sound
+
+
+def whole_state(p: OraclePool):
+    """Every field of the oracle's state (S:132 / S:169 / S:178 'pool unchanged' is checked against all of it)."""
+    import copy
+    return (p.store.pool.copy(), p.store.host.copy(), p.blk_state.copy(), p.owner.copy(),
+            {a: (g.cls, list(g.table)) for a, g in p.agents.items()}, list(p.reserved), list(p.claimed),
+            list(p.slot_free), list(p.peer_free), list(p.released_slots), list(p.released_epoch),
+            copy.deepcopy(p.pending_dev), list(p.pending_epoch), p.epoch, p.next_handle,
+            {h: (x.agent, x.cls, x.state, list(x.pos), list(x.slots), list(x.resv), list(x.plan), x.ticks)
+             for h, x in p.handles.items()})
+
+
+def states_equal(a, b):
+    if isinstance(a, np.ndarray):
+        return np.array_equal(a, b)
+    if isinstance(a, (tuple, list)):
+        return len(a) == len(b) and all(states_equal(x, y) for x, y in zip(a, b))
+    if isinstance(a, dict):
+        return a.keys() == b.keys() and all(states_equal(a[k], b[k]) for k in a)
+    return a == b
 
 
 def test_round_trip_identity_explicit():
