@@ -41,3 +41,22 @@ def test_contents_cover_special_fp_patterns():
     assert ((exp_bf16 == 0xFF) & ((w & 0x7F) != 0)).any()      # bf16 NaN
     assert (exp_bf16 == 0).any()                                # bf16 zero/denormal
     assert ((w == 0x8000)).sum() >= 0
+
+
+def test_torch_generator_matches_numpy_generator():
+    """tests/gen_torch.py (the full-size GPU tests' expected-bytes generator) equals this module on CPU: the
+    reference outputs, and whole shard blocks with scattered provenance for every head split."""
+    import torch
+    from gen_torch import _i64, block_words, splitmix64
+    g = 0x9E3779B97F4A7C15
+    xs = torch.tensor([_i64(0), _i64(g), _i64(2 * g)], dtype=torch.int64)
+    assert [v & ((1 << 64) - 1) for v in splitmix64(xs).tolist()] == [0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4,
+                                                                      0x06C45D188009454F]
+    L, N, T, H, D = 3, 40, 16, 8, 64
+    provs = torch.tensor([0, 39, 17, 5, 5, 22], dtype=torch.int64)
+    for seed in (0, 3, 12345):
+        for world in (1, 2, 8):
+            for rank in {0, world - 1}:
+                full = content.pool_bytes(seed, L, N, T, H, D, rank=rank, world=world)
+                got = block_words(seed, provs, L, N, T, H, D, rank, world).numpy().view(np.uint8)
+                assert np.array_equal(got, full[:, :, provs.numpy()]), (seed, world, rank)

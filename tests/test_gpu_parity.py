@@ -3,8 +3,7 @@
 * small pools (C1 and fuzz scripts, several geometries with ragged chunk counts): the whole device pool, every live
   handle's pinned host image, every block table (host mirror and device table) and all counters are compared
   after every sync, in both transfer modes (DIRECT mapped-host kernels, STAGED device ring + copy engine);
-* full BASELINE sizes (C2..C5 shard, in the launch configuration bench.py times): tables and counters in full, KV
-  bytes on sampled (layer, K|V, block) chunks against the generator at the oracle's provenance;
+* full BASELINE sizes: tests/test_gpu_fullsize.py;
 * the synthetic-content fill kernel against workloads/content.py; the device tier against numpy.take.
 """
 import numpy as np
@@ -15,7 +14,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_2510_18586_b200 as tcb  # noqa: E402
-from oracle import BytesStore, OraclePool, ProvStore  # noqa: E402
+from oracle import BytesStore, OraclePool  # noqa: E402
 from oracle.pool import OFFLOADED  # noqa: E402
 from workloads import content  # noqa: E402
 from workloads.configs import CONFIGS  # noqa: E402
@@ -38,11 +37,11 @@ def _cuda():
 
 
 def dev_pool(L, H, D, N, S, mode="direct", ncls=N_CLASSES, max_bpa=4096, seed=1, rank=0, world=1, staging=0,
-             dtype="bf16", T=16, P=0):
+             dtype="bf16", T=16, P=0, peer_dev=0):
     d2h, h2d, variant = MODES[mode]
     p = tcb.Pool(L, H, D, T, dtype, N, device=0, shard_rank=rank, shard_world=world, host_slots=S, n_classes=ncls,
                  max_agents=1024, max_blocks_per_agent=max_bpa, xfer_d2h=d2h, xfer_h2d=h2d, staging_bytes=staging,
-                 peer_device=0 if P else -1, peer_slots=P)
+                 peer_device=peer_dev if P else -1, peer_slots=P)
     for path in range(3):
         p.set_launch_config(path, 0, 256, variant)
     p.fill(seed)
@@ -72,11 +71,11 @@ def compare_live_host(o: OraclePool, c: tcb.Pool, where=""):
             assert np.array_equal(c.handle_host_bytes(h, i), o.store.host[s]), (where, h, i)
 
 
-def run_script(ops, L, H, D, N, S, mode, ncls=N_CLASSES, max_bpa=4096, seed=1, staging=0, T=16, P=0):
+def run_script(ops, L, H, D, N, S, mode, ncls=N_CLASSES, max_bpa=4096, seed=1, staging=0, T=16, P=0, peer_dev=0):
     pool0 = content.pool_bytes(seed, L, N, T, H, D)
     o = OraclePool(N, S, n_classes=ncls, max_agents=1024, max_blocks_per_agent=max_bpa,
                    store=BytesStore(pool0, S + P), n_peer_slots=P)
-    c = dev_pool(L, H, D, N, S, mode, ncls, max_bpa, seed, staging=staging, T=T, P=P)
+    c = dev_pool(L, H, D, N, S, mode, ncls, max_bpa, seed, staging=staging, T=T, P=P, peer_dev=peer_dev)
     assert np.array_equal(c.kv_tensor().cpu().numpy(), pool0), "fill kernel != content generator"
     ro, rc = Replayer(o), Replayer(c)
     for i, op in enumerate(ops):
@@ -168,61 +167,7 @@ def test_special_bit_patterns_survive_round_trip():
     assert np.array_equal(after[:, :, new], before[:, :, ids])
 
 
-# --------------------------------------------------------------------------------------- full BASELINE sizes
-def sample_check(c: tcb.Pool, cfg, prov: np.ndarray, blocks: np.ndarray, seed: int, rank: int, world: int,
-                 rng, per_block: int = 2):
-    L = cfg.L
-    kvt = c.kv_tensor()
-    lk = rng.integers(0, 2 * L, size=(len(blocks), per_block))
-    bl = np.repeat(blocks, per_block)
-    lk = lk.reshape(-1)
-    got = kvt[torch.from_numpy(lk // 2).cuda(), torch.from_numpy(lk % 2).cuda(),
-              torch.from_numpy(bl.astype(np.int64)).cuda()].cpu().numpy()
-    for k in range(len(bl)):
-        exp = content.chunk_bytes(seed, int(lk[k] // 2), int(lk[k] % 2), int(prov[bl[k]]), cfg.N, cfg.T, cfg.H,
-                                  cfg.D, rank=rank, world=world)
-        assert np.array_equal(got[k], exp), (cfg.name, int(bl[k]), int(lk[k]))
-
-
-@pytest.mark.parametrize("name,world,lag", [("c2", 1, 1), ("c3", 1, 1), ("c4", 1, 1), ("c4", 8, 1), ("c5", 8, 1),
-                                            ("c2", 1, 4), ("c3", 1, 2)])
-def test_full_size_config_parity(name, world, lag):
-    """Full-size pools in bench.py's launch configuration: tc_cycle + tc_retire_lag(lag) per cycle (lag 1 =
-    tc_retire), byte parity on sampled chunks against the oracle's provenance, tables and counters exact."""
-    cfg = CONFIGS[name]
-    rank = world - 1 if world > 1 else 0
-    S = cfg.host_slots()
-    ops = build_script(cfg, 8, combined=True)          # tc_cycle + tc_retire per scheduling cycle, as bench.py times it
-    n_setup = next(i for i, op in enumerate(ops) if op[0] == "cycle")
-    rt = ("retire",) if lag == 1 else ("retire", lag)
-    ops = ops[:n_setup] + [rt if op[0] == "sync" else ("cycle_r",) + op[1:] if op[0] == "cycle" else op
-                           for op in ops[n_setup:]] + [("sync",)]
-    o = OraclePool(cfg.N, S, max_agents=1024, max_blocks_per_agent=cfg.max_blocks_per_agent,
-                   store=ProvStore(cfg.N, S))
-    c = tcb.Pool(cfg.L, cfg.H, cfg.D, cfg.T, cfg.dtype, cfg.N, device=0, shard_rank=rank, shard_world=world,
-                 host_slots=S, max_agents=1024, max_blocks_per_agent=cfg.max_blocks_per_agent)
-    c.fill(cfg.seed)
-    ro, rc = Replayer(o), Replayer(c)
-    touched = set()
-    for i, op in enumerate(ops):
-        a, b = ro.step(op), rc.step(op)
-        assert a == b, (i, op)
-        assert a[0] == 0, (i, op)
-        if op[0] in ("cycle", "cycle_r") and a[1]:
-            for ids in a[1][0]:
-                touched.update(ids)
-    c.sync()
-    tab = c.table_tensor().cpu().numpy()
-    for ag_id, ag in o.agents.items():
-        assert c.block_table(ag_id) == ag.table
-        assert tab[ag_id, :len(ag.table)].tolist() == ag.table
-    rng = np.random.default_rng(cfg.seed)
-    touched = np.array(sorted(touched), dtype=np.int64)
-    assert len(touched) > 0
-    sample_check(c, cfg, o.store.prov, touched, cfg.seed, rank, world, rng)
-    others = rng.choice(cfg.N, size=512, replace=False)
-    sample_check(c, cfg, o.store.prov, others, cfg.seed, rank, world, rng)
-    c.close()
+# full BASELINE sizes: tests/test_gpu_fullsize.py (whole pool + every live host image, exhaustive)
 
 
 @pytest.mark.parametrize("head_kib,piece_kib", [(0, 2), (1, 2), (3, 1024), (64, 64), (4096, 1024)])
@@ -288,6 +233,26 @@ def test_peer_tier_fuzz_bytes(mode, gi):
         ops = fuzz_script(seed + 31 * gi, n_ops=90, n_agents=3, n_classes=N_CLASSES, N=N, max_alloc=6)
         o, c = run_script(ops, L, H, D, N, S, mode, seed=seed + 5, T=T, P=max(2, S // 2))
         assert c.stats()["peer_slots"] == max(2, S // 2)
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="NEXT-2 across GPUs needs a second GPU (the peer slab in its HBM, reached over NVLink)")
+@pytest.mark.parametrize("mode", ["staged", "direct"])
+def test_peer_tier_on_second_gpu(mode):
+    """NEXT-2 peer tier (reading C1) with the peer slab in GPU 1's HBM: offloads gather straight into the
+    neighbour's memory over NVLink (peer access), uploads scatter back from it; pool bytes, peer / host images,
+    tables and counters against the oracle after every sync, for fuzz scripts and C2-shaped tc_cycle batches."""
+    for gi in (0, 2):
+        L, H, D, N, S, T = GEOMS[gi]
+        for seed in range(2):
+            ops = fuzz_script(seed + 71 * gi, n_ops=90, n_agents=3, n_classes=N_CLASSES, N=N, max_alloc=6)
+            o, c = run_script(ops, L, H, D, N, S, mode, seed=seed + 5, T=T, P=max(2, S // 2), peer_dev=1)
+            c.close()
+    cfg = CONFIGS["c2"].scaled(N=512, host_slots=160, bg_fill=0.3)
+    o, c = run_script(build_script(cfg, 10, combined=True), cfg.L, cfg.H, cfg.D, cfg.N, cfg.host_slots(), mode,
+                      seed=2, P=96, peer_dev=1)
+    assert any(x >= cfg.host_slots() for h in o.handles.values() for x in h.slots)
+    c.close()
 
 
 def test_peer_tier_cycles_mixed_tiers():
