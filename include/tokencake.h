@@ -154,7 +154,10 @@ tc_status tc_calibrate(tc_pool *p, int64_t probe_bytes, tc_calibration_t *out);
    variant 0 = SIMT warp-per-chunk 16-byte copies, 1 = TMA bulk copies (cp.async.bulk through an 8-stage
    shared-memory ring, one elected thread per CTA, one CTA per SM), 2 = SIMT tile split (4 KiB warp tiles spread
    evenly over all CTAs), 3 = TMA bulk with a 4-stage ring (two CTAs per SM).  Other values -> TC_E_INVAL.
-   Results are identical for every setting; only speed differs. */
+   Results are identical for every setting; only speed differs.  Defaults (at create; TC_CTAS_* / TC_VARIANT_*
+   override): variant 3 on every path; 32 CTAs for path 0, 74 for path 1 (a DIRECT kernel occupies its SMs for the
+   whole link transfer, so it gets a small fixed grid that leaves the other direction room), the size-adaptive grid
+   (ctas = 0) for paths 2 and 3.  ctas <= 0 here restores the variant's size-adaptive grid. */
 tc_status tc_set_launch_config(tc_pool *p, int32_t path, int32_t ctas, int32_t threads, int32_t variant);
 /* Synthetic content: every 8-byte word of the unsharded pool = splitmix64(widx + seed*0xD1B54A32D192ED03), widx its
    index in [L][2][N][T][H][D]; this rank writes its head shard.  Tests/bench only. */

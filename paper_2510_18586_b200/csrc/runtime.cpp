@@ -235,15 +235,21 @@ tc_status Pool::create(const tc_pool_desc &d) {
     peer.device = d.peer_device;
     peer.free_list.resize(peer.count);
     for (int64_t i = 0; i < peer.count; ++i) peer.free_list[i] = S + peer.count - 1 - i;
+    // Default launch configuration per path: TMA bulk everywhere.  The DIRECT kernels move bytes over
+    // the host link for the whole transfer, so they get a fixed small grid — 32 CTAs for the mapped-host writes
+    // (D2H), 74 for the reads (H2D) — that leaves the other direction's kernel and the engine's compute room on the
+    // SMs; the old 592 x 256-thread SIMT grid filled every register file, so a concurrent D2H and H2D ran one after
+    // the other (profiles/r02_direct_probe_c2_*.json).  Device side / peer tier: the size-adaptive grid (0).
     const char *path_names[4] = {"D2H", "H2D", "DEV", "PEER"};
+    const int default_ctas[4] = {32, 74, 0, 0};
     for (int i = 0; i < 4; ++i) {
         char nm[32];
         std::snprintf(nm, sizeof nm, "TC_CTAS_%s", path_names[i]);
-        ctas[i] = env_int(nm, 0);
+        ctas[i] = env_int(nm, default_ctas[i]);
         std::snprintf(nm, sizeof nm, "TC_THREADS_%s", path_names[i]);
         nthreads[i] = env_int(nm, 256);
         std::snprintf(nm, sizeof nm, "TC_VARIANT_%s", path_names[i]);
-        variant[i] = env_int(nm, i >= 2 ? 3 : 0);   // device side and peer tier: TMA bulk
+        variant[i] = env_int(nm, 3);
     }
     if (meta_only) return TC_OK;
 

@@ -27,7 +27,8 @@ MODES = {"direct": (tcb.XFER_DIRECT, tcb.XFER_DIRECT, 0), "staged": (tcb.XFER_ST
          "staged_tile": (tcb.XFER_STAGED, tcb.XFER_STAGED, 2), "staged_tma4": (tcb.XFER_STAGED, tcb.XFER_STAGED, 3),
          "mixed_rev": (tcb.XFER_STAGED, tcb.XFER_DIRECT, 2), "copy": (tcb.XFER_COPY, tcb.XFER_COPY, 0),
          "copy_staged": (tcb.XFER_COPY, tcb.XFER_STAGED, 3), "staged_copy": (tcb.XFER_STAGED, tcb.XFER_COPY, 3),
-         "auto": (tcb.XFER_AUTO, tcb.XFER_AUTO, 3)}
+         "auto": (tcb.XFER_AUTO, tcb.XFER_AUTO, 3), "direct_tma4": (tcb.XFER_DIRECT, tcb.XFER_DIRECT, 3),
+         "direct_default": (tcb.XFER_DIRECT, tcb.XFER_DIRECT, None)}
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -42,8 +43,9 @@ def dev_pool(L, H, D, N, S, mode="direct", ncls=N_CLASSES, max_bpa=4096, seed=1,
     p = tcb.Pool(L, H, D, T, dtype, N, device=0, shard_rank=rank, shard_world=world, host_slots=S, n_classes=ncls,
                  max_agents=1024, max_blocks_per_agent=max_bpa, xfer_d2h=d2h, xfer_h2d=h2d, staging_bytes=staging,
                  peer_device=peer_dev if P else -1, peer_slots=P)
-    for path in range(3):
-        p.set_launch_config(path, 0, 256, variant)
+    if variant is not None:                 # None: the library's default launch configuration per path
+        for path in range(3):
+            p.set_launch_config(path, 0, 256, variant)
     p.fill(seed)
     return p
 

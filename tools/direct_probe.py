@@ -27,6 +27,9 @@ def main():
     ap.add_argument("--geom", default="c2")
     ap.add_argument("--reps", type=int, default=6)
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--focus", action="store_true",
+                    help="candidate configs only: each direction alone and both together, and the mixed pairs "
+                         "(direct D2H + staged H2D, staged D2H + direct H2D)")
     a = ap.parse_args()
     L, H, D, G = GEOMS[a.geom]
     NB = a.blocks
@@ -48,7 +51,8 @@ def main():
     offs = torch.cuda.ExternalStream(off_s, device=0)
     res = []
 
-    def one(cfg):
+    def one(cfg, modes=(tcb.XFER_DIRECT, tcb.XFER_DIRECT), which="both"):
+        p.set_xfer_mode(*modes)
         for path in (0, 1):
             p.set_launch_config(path, *cfg[path])
         h = p.offload(0, p.block_table(0))     # agent 0 on the host: its upload runs beside agent 1's offload
@@ -61,7 +65,7 @@ def main():
             e1u, e1o = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0u.record(ups)
             e0o.record(offs)
-            _, hs = p.cycle([h], [(1, p.block_table(1))])
+            _, hs = p.cycle([h] if which != "off" else [], [(1, p.block_table(1))] if which != "up" else [])
             e1u.record(ups)
             e1o.record(offs)
             p.sync()
@@ -69,22 +73,51 @@ def main():
             wall = max(e0u.elapsed_time(e1u), e0u.elapsed_time(e1o), e0o.elapsed_time(e1u), e0o.elapsed_time(e1o))
             off_ms, off_n, off_b = tim["dev_offload_direct_kernel"]
             up_ms, up_n, up_b = tim["dev_upload_direct_kernel"]
-            h = hs[0]
-            p.upload(h)                        # agent 1 back on the GPU (the next rep offloads it again)
-            p.sync()
-            h = p.offload(0, p.block_table(0))
-            p.sync()
+            moved = (NB * B if which != "up" else 0) + (NB * B if which != "off" else 0)
+            if which != "up":
+                p.upload(hs[0])                # agent 1 back on the GPU (the next rep offloads it again)
+                p.sync()
+            if which != "off":
+                h = p.offload(0, p.block_table(0))
+                p.sync()
             if rep:
                 rows.append({"off_gbs": off_b / (off_ms * 1e-3) / 1e9 if off_ms else None,
                              "up_gbs": up_b / (up_ms * 1e-3) / 1e9 if up_ms else None,
-                             "cycle_gbs": (off_b + up_b) / (wall * 1e-3) / 1e9, "cycle_ms": wall,
-                             "off_ms": off_ms, "up_ms": up_ms})
+                             "cycle_gbs": moved / (wall * 1e-3) / 1e9, "cycle_ms": wall,
+                             "off_ms": off_ms or None, "up_ms": up_ms or None})
         p.upload(h)
         p.sync()
-        med = {k: float(np.median([r[k] for r in rows if r[k] is not None])) for k in rows[0]}
+        med = {k: float(np.median([r[k] for r in rows if r[k] is not None])) for k in rows[0]
+               if any(r[k] is not None for r in rows)}
         # overlap: if the kernels ran one after the other, cycle_ms ~ off_ms + up_ms; fully overlapped ~ max(..)
-        med["serial_fraction"] = (med["cycle_ms"] - max(med["off_ms"], med["up_ms"])) / min(med["off_ms"], med["up_ms"])
+        if "off_ms" in med and "up_ms" in med:
+            med["serial_fraction"] = (med["cycle_ms"] - max(med["off_ms"], med["up_ms"])) / min(med["off_ms"],
+                                                                                               med["up_ms"])
         return med
+
+    if a.focus:
+        names = {tcb.XFER_DIRECT: "direct", tcb.XFER_STAGED: "staged"}
+        cands = [(592, 128, 0), (296, 256, 0), (74, 256, 0), (74, 32, 3), (32, 32, 3), (16, 32, 3), (74, 32, 1),
+                 (148, 32, 3)]
+        D, St = tcb.XFER_DIRECT, tcb.XFER_STAGED
+        for cand in cands:
+            cfg = {0: cand, 1: cand}
+            for modes, which in (((D, D), "off"), ((D, D), "up"), ((D, D), "both"), ((D, St), "both"),
+                                 ((St, D), "both")):
+                med = one(cfg, modes, which)
+                r = {"geom": a.geom, "blocks": NB, "cfg": list(cand), "d2h": names[modes[0]], "h2d": names[modes[1]],
+                     "which": which, **{k: round(v, 3) for k, v in med.items()}}
+                res.append(r)
+                print(json.dumps(r), flush=True)
+        med = one({0: cands[0], 1: cands[0]}, (St, St), "both")
+        r = {"geom": a.geom, "blocks": NB, "d2h": "staged", "h2d": "staged", "which": "both",
+             **{k: round(v, 3) for k, v in med.items()}}
+        res.append(r)
+        print(json.dumps(r), flush=True)
+        os.makedirs("gpurun_out", exist_ok=True)
+        with open(f"gpurun_out/direct_focus_{a.geom}.json", "w") as f:
+            json.dump(res, f, indent=1)
+        return
 
     grid_set = (16, 32, 74, 148, 296, 592) if not a.quick else (32, 148, 592)
     cfgs = []
