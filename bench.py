@@ -727,11 +727,13 @@ def run_ours(args):
 def ncu_traffic(cfg_name, kind, kd):
     """roofline.traffic for the staged HBM kernels: DRAM bytes per launch from the committed `ncu --set full` capture
     of fixed-size launches of the same kernel on the same config (tools/traffic_probe.py -> profiles/
-    r01_traffic_<cfg>.json), as the captured ratio (dram read + write) / algorithmic bytes times this run's per-launch
+    r<round>_traffic_<cfg>.json, the latest round's), as the captured ratio (dram read + write) / algorithmic bytes times this run's per-launch
     algorithmic bytes.  None when no capture exists or the kernel is a host-link one."""
-    path = os.path.join(ROOT, "profiles", f"r01_traffic_{cfg_name}.json")
-    if kd.get("bound") != "hbm" or not os.path.exists(path):
+    caps = [os.path.join(ROOT, "profiles", f"r{r:02d}_traffic_{cfg_name}.json") for r in (2, 1)]
+    caps = [c for c in caps if os.path.exists(c)]                 # the latest round's capture first
+    if kd.get("bound") != "hbm" or not caps:
         return {}
+    path = caps[0]
     cap = [x for x in json.load(open(path))["launches"] if x["kind"] == kind]
     if not cap:
         return {}

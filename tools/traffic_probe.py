@@ -1,5 +1,5 @@
 """Fixed-size device-side gather + scatter launches for an `ncu --set full` DRAM-traffic capture (GPU box):
-  ncu --set full -k regex:k_xfer_bulk -o gpurun_out/prof_traffic python tools/traffic_probe.py [config]
+  ncu --set full -k regex:k_xfer_bulk -o gpurun_out/prof_traffic python tools/traffic_probe.py [config [MiB]]
 Each launch moves a known number of blocks, so its algorithmic bytes (2 x n x B: read + write) are exact; the
 capture's dram__bytes_read/write per launch divided by them is the traffic ratio bench.py reports."""
 import json
@@ -22,7 +22,8 @@ def main():
     p = tcb.Pool(cfg.L, cfg.H, cfg.D, cfg.T, cfg.dtype, N, device=0, shard_world=G, host_slots=16)
     p.fill(3)
     B = p.block_bytes
-    n = max(1, (112 << 20) // B)                    # ~ one C2 scheduling cycle's offload
+    mib = int(sys.argv[2]) if len(sys.argv) > 2 else 112   # default ~ one C2 scheduling cycle's offload
+    n = max(1, (mib << 20) // B)
     ids = np.random.default_rng(7).choice(N, size=n, replace=False).astype(np.int32)
     dst = torch.empty(n * B, dtype=torch.uint8, device="cuda:0")
     for _ in range(2):
