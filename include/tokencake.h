@@ -153,7 +153,8 @@ tc_status tc_calibrate(tc_pool *p, int64_t probe_bytes, tc_calibration_t *out);
    threads in {32..256} (SIMT variants);
    variant 0 = SIMT warp-per-chunk 16-byte copies, 1 = TMA bulk copies (cp.async.bulk through an 8-stage
    shared-memory ring, one elected thread per CTA, one CTA per SM), 2 = SIMT tile split (4 KiB warp tiles spread
-   evenly over all CTAs), 3 = TMA bulk with a 4-stage ring (two CTAs per SM).  Other values -> TC_E_INVAL.
+   evenly over all CTAs), 3 = TMA bulk with a 4-stage ring (two CTAs per SM), 4 = SIMT tiles of 32-byte vectors with
+   the L2::256B fetch hint (C % 32 == 0, else as 2).  Other values -> TC_E_INVAL.
    Results are identical for every setting; only speed differs.  Defaults (at create; TC_CTAS_* / TC_VARIANT_*
    override): variant 3 on every path; 32 CTAs for path 0, 74 for path 1 (a DIRECT kernel occupies its SMs for the
    whole link transfer, so it gets a small fixed grid that leaves the other direction room), the size-adaptive grid

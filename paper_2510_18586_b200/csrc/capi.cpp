@@ -139,7 +139,7 @@ tc_status tc_calibrate(tc_pool *p, int64_t probe_bytes, tc_calibration_t *out) {
 
 tc_status tc_set_launch_config(tc_pool *p, int32_t path, int32_t ctas, int32_t threads, int32_t variant) {
     TC_GUARD(p) {
-        if (path < 0 || path > 3 || threads < 32 || threads > 256 || threads % 32 || variant < 0 || variant > 3)
+        if (path < 0 || path > 3 || threads < 32 || threads > 256 || threads % 32 || variant < 0 || variant > 4)
             return TC_E_INVAL;
         P.ctas[path] = ctas;
         P.nthreads[path] = threads;

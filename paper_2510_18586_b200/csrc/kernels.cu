@@ -16,6 +16,7 @@
 //   1  TMA bulk, one elected thread per CTA streams 16 KiB pieces through an 8-stage shared-memory ring (1 CTA/SM)
 //   2  SIMT, the launch's chunks cut into 4 KiB warp tiles split evenly over all CTAs
 //   3  TMA bulk, 4-stage ring (2 CTAs/SM)
+//   4  SIMT, 8 KiB warp tiles of 32-byte vectors with the L2::256B fetch hint (C % 32 == 0; else variant 2)
 // Work is split over CTAs at piece/tile granularity (variants 1-3), so a small launch (the staged head/tail piece)
 // still reaches every SM and a large one has no chunk-granular tail.
 #include <algorithm>
@@ -150,6 +151,67 @@ __device__ __forceinline__ void tile_body(const XferDesc *__restrict__ desc, int
             for (int u = 0; u < kTileU; ++u) st_stream(dst + lane + 32 * u, v[u]);
         } else {
             for (int64_t v = lane; v < nv; v += 32) st_stream(dst + v, ld_stream(src + v));
+        }
+        if (r == 0 && lane == 0 && d.tab >= 0) table[d.tab] = kGather ? -1 : d.blk;
+    }
+    if (g.ts) {
+        __syncthreads();
+        if (threadIdx.x == 0) ts_end(g);
+    }
+}
+
+// ------------------------------------------------------------------------------------------------ variant 4
+// SIMT tile split like variant 2 with 32-byte vectors (LDG/STG .256) and the L2::256B fetch-size hint on the loads:
+// a warp iteration moves 32 lanes x kTileU x 32 B = 8 KiB.  Meant for mapped host memory, where the size of each
+// sysmem request may decide how many requests the link carries.  Needs C % 32 == 0 (else the launch uses variant 2).
+struct V8 {
+    uint32_t r[8];
+};
+__device__ __forceinline__ V8 ld_stream8(const V8 *p) {
+    V8 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v.r[0]), "=r"(v.r[1]), "=r"(v.r[2]), "=r"(v.r[3]), "=r"(v.r[4]), "=r"(v.r[5]), "=r"(v.r[6]),
+                   "=r"(v.r[7])
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_stream8(V8 *p, const V8 &v) {
+    asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.r[0]),
+                 "r"(v.r[1]), "r"(v.r[2]), "r"(v.r[3]), "r"(v.r[4]), "r"(v.r[5]), "r"(v.r[6]), "r"(v.r[7])
+                 : "memory");
+}
+constexpr int64_t kTile8Bytes = kTileU * 32 * 32;
+
+template <bool kGather>
+__device__ __forceinline__ void tile8_body(const XferDesc *__restrict__ desc, int64_t n, const XferGeom &g,
+                                           char *__restrict__ kv, int32_t *__restrict__ table, int64_t per_cta) {
+    const int64_t tpc = (g.chunk + kTile8Bytes - 1) / kTile8Bytes;
+    const int64_t tpb = tpc * g.two_l;
+    const int64_t Mt = n * tpb;
+    const int64_t t0 = (int64_t)blockIdx.x * per_cta;
+    if (t0 >= Mt) return;
+    if (threadIdx.x == 0) ts_begin(g);
+    const int64_t t1 = min(Mt, t0 + per_cta);
+    const int lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x >> 5;
+    for (int64_t t = t0 + (threadIdx.x >> 5); t < t1; t += nwarps) {
+        const int64_t i = t / tpb;
+        const int64_t r = t - i * tpb;
+        const int64_t lk = r / tpc;
+        const int64_t off = (r - lk * tpc) * kTile8Bytes;
+        const XferDesc d = desc[i];
+        const Loc p = locate(d, lk, off, g, kv);
+        const V8 *src = reinterpret_cast<const V8 *>(kGather ? p.pool : p.ext);
+        V8 *dst = reinterpret_cast<V8 *>(kGather ? p.ext : p.pool);
+        const int64_t nv = min(kTile8Bytes, g.chunk - off) >> 5;
+        if (nv == kTileU * 32) {
+            V8 v[kTileU];
+#pragma unroll
+            for (int u = 0; u < kTileU; ++u) v[u] = ld_stream8(src + lane + 32 * u);
+#pragma unroll
+            for (int u = 0; u < kTileU; ++u) st_stream8(dst + lane + 32 * u, v[u]);
+        } else {
+            for (int64_t v = lane; v < nv; v += 32) st_stream8(dst + v, ld_stream8(src + v));
         }
         if (r == 0 && lane == 0 && d.tab >= 0) table[d.tab] = kGather ? -1 : d.blk;
     }
@@ -295,6 +357,13 @@ __global__ void __launch_bounds__(256) k_xfer_tile(const __grid_constant__ Descs
 }
 
 template <bool kGather, int kCap>
+__global__ void __launch_bounds__(256) k_xfer_tile8(const __grid_constant__ Descs<kCap> dd, int32_t n, XferGeom g,
+                                                    char *__restrict__ kv, int32_t *__restrict__ table,
+                                                    int64_t per_cta) {
+    tile8_body<kGather>(dd.d, n, g, kv, table, per_cta);
+}
+
+template <bool kGather, int kCap>
 __global__ void __launch_bounds__(32) k_xfer_bulk(const __grid_constant__ Descs<kCap> dd, int32_t n, XferGeom g,
                                                   char *__restrict__ kv, int32_t *__restrict__ table,
                                                   int64_t per_cta, int32_t piece, int32_t stages) {
@@ -340,6 +409,16 @@ cudaError_t launch_cap(bool gather, const XferDesc *host_desc, int32_t n, const 
     }
     if (threads <= 0 || threads > 256) threads = 256;
     const int64_t nwarps = threads / 32;
+    if (variant == 4 && g.chunk % 32 == 0) {
+        const int64_t Mt = (int64_t)n * g.two_l * ((g.chunk + kTile8Bytes - 1) / kTile8Bytes);
+        split(Mt, ctas > 0 ? ctas : 148 * 4, nwarps, &grid, &per);
+        if (gather)
+            k_xfer_tile8<true, kCap><<<(unsigned)grid, threads, 0, s>>>(dd, n, g, kv, table, per);
+        else
+            k_xfer_tile8<false, kCap><<<(unsigned)grid, threads, 0, s>>>(dd, n, g, kv, table, per);
+        return cudaGetLastError();
+    }
+    if (variant == 4) variant = 2;                   // C % 32 != 0: 16-byte tiles
     if (variant == 2) {
         const int64_t Mt = (int64_t)n * g.two_l * ((g.chunk + kTileBytes - 1) / kTileBytes);
         split(Mt, ctas > 0 ? ctas : 148 * 4, nwarps, &grid, &per);
@@ -402,7 +481,7 @@ __global__ void k_fill(uint64_t *__restrict__ kv, int64_t n_chunks, int64_t n_po
 cudaError_t launch_xfer(bool gather, const XferDesc *host_desc, int32_t n, const XferGeom &g, void *kv,
                         int32_t *table, int ctas, int threads, int variant, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
-    if (n > kMaxInlineDesc || variant < 0 || variant > 3) return cudaErrorInvalidValue;
+    if (n > kMaxInlineDesc || variant < 0 || variant > 4) return cudaErrorInvalidValue;
     char *k = static_cast<char *>(kv);
     if (n <= 64) return launch_cap<64>(gather, host_desc, n, g, k, table, ctas, threads, variant, s);
     if (n <= 256) return launch_cap<256>(gather, host_desc, n, g, k, table, ctas, threads, variant, s);

@@ -32,7 +32,7 @@ struct XferGeom {
 // host_desc: n <= kMaxInlineDesc descriptors in host memory, copied into the launch's parameters.  ctas <= 0 selects
 // the variant's default grid.  variant 0 = SIMT warp-per-chunk 16-byte copy; 1 = TMA bulk (cp.async.bulk) through
 // an 8-stage shared-memory ring, one CTA per SM; 2 = SIMT tile split (4 KiB warp tiles spread evenly over all CTAs);
-// 3 = TMA bulk, 4-stage ring, two CTAs per SM.
+// 3 = TMA bulk, 4-stage ring, two CTAs per SM; 4 = SIMT 8 KiB tiles of 32-byte vectors (L2::256B; C % 32 == 0).
 cudaError_t launch_xfer(bool gather, const XferDesc *host_desc, int32_t n, const XferGeom &g, void *kv,
                         int32_t *table, int ctas, int threads, int variant, cudaStream_t s);
 

@@ -28,7 +28,8 @@ MODES = {"direct": (tcb.XFER_DIRECT, tcb.XFER_DIRECT, 0), "staged": (tcb.XFER_ST
          "mixed_rev": (tcb.XFER_STAGED, tcb.XFER_DIRECT, 2), "copy": (tcb.XFER_COPY, tcb.XFER_COPY, 0),
          "copy_staged": (tcb.XFER_COPY, tcb.XFER_STAGED, 3), "staged_copy": (tcb.XFER_STAGED, tcb.XFER_COPY, 3),
          "auto": (tcb.XFER_AUTO, tcb.XFER_AUTO, 3), "direct_tma4": (tcb.XFER_DIRECT, tcb.XFER_DIRECT, 3),
-         "direct_default": (tcb.XFER_DIRECT, tcb.XFER_DIRECT, None)}
+         "direct_default": (tcb.XFER_DIRECT, tcb.XFER_DIRECT, None),
+         "direct_tile8": (tcb.XFER_DIRECT, tcb.XFER_DIRECT, 4), "staged_tile8": (tcb.XFER_STAGED, tcb.XFER_STAGED, 4)}
 
 
 @pytest.fixture(scope="module", autouse=True)

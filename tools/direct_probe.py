@@ -98,7 +98,9 @@ def main():
     if a.focus:
         names = {tcb.XFER_DIRECT: "direct", tcb.XFER_STAGED: "staged"}
         cands = [(592, 128, 0), (296, 256, 0), (74, 256, 0), (74, 32, 3), (32, 32, 3), (16, 32, 3), (74, 32, 1),
-                 (148, 32, 3)]
+                 (148, 32, 3), (74, 256, 4), (148, 256, 4), (296, 256, 4), (592, 128, 4)]
+        if os.environ.get("DP_CANDS"):                # e.g. DP_CANDS="74,256,4;148,256,4"
+            cands = [tuple(int(x) for x in c.split(",")) for c in os.environ["DP_CANDS"].split(";")]
         D, St = tcb.XFER_DIRECT, tcb.XFER_STAGED
         for cand in cands:
             cfg = {0: cand, 1: cand}
