@@ -554,7 +554,7 @@ def run_ours(args):
                 f.write(json.dumps(r) + "\n")
     diag = pool.timing(0)
     tl_raw = pool.timeline(200000)
-    other = per_cycle_drain(torch, dev, cycle, ups, offs_, B, min(args.steps, 40), flush) if args.retire == "each" \
+    other = per_cycle_drain(torch, dev, cycle, ups, offs_, B, min(args.steps, 40), flush, link) if args.retire == "each" \
         else None
     tl_summary = timeline_summary(tl_raw)
     if os.environ.get("TC_DUMP_TIMELINE"):                 # debugging aid: raw per-span records of the diagnostic steps
@@ -647,10 +647,7 @@ def run_ours(args):
             how = ("all steps: max(total up / H2D peak, total off / D2H peak, total / bidirectional peak), the link's "
                    "lower bound for any schedule, vs the measured time")
         else:
-            for u, o in step_bytes:
-                lo, hi = min(u, o), max(u, o)
-                uni = link["h2d_gbs"] if u >= o else link["d2h_gbs"]
-                tmin += lo / (bi * 1e9) + (hi - lo) / (uni * 1e9)
+            tmin = sum(step_link_bound_s(u, o, link) for u, o in step_bytes)
             how = ("per step: min(up,off) at half the measured bidirectional peak + the excess at the unidirectional "
                    "peak, vs the measured step time")
         link_roof = {"bound": "host_link", "step_min_ms": tmin * 1e3 / len(step_bytes),
@@ -744,10 +741,19 @@ def ncu_traffic(cfg_name, kind, kd):
                                "note": "ncu counts writes still dirty in L2 at kernel end as not yet written"}}
 
 
-def per_cycle_drain(torch, dev, cycle, ups, offs, B, n, flush):
+def step_link_bound_s(up: float, off: float, link: dict) -> float:
+    """The host link's lower bound (s) for one drained step moving `up` bytes H2D and `off` bytes D2H: the smaller
+    direction at half the measured bidirectional peak, the excess at the unidirectional peak of the larger one."""
+    lo, hi = min(up, off), max(up, off)
+    uni = link["h2d_gbs"] if up >= off else link["d2h_gbs"]
+    return lo / (link["bidir_gbs"] / 2 * 1e9) + (hi - lo) / (uni * 1e9)
+
+
+def per_cycle_drain(torch, dev, cycle, ups, offs, B, n, flush, link=None):
     """Diagnostic (not `value`): the same cycles run with a tc_sync each (drain and retire every cycle, L2 flushed
-    between them); device time per cycle from just before tc_cycle to the end of both copy streams' work."""
-    tot_ms, moved = 0.0, 0
+    between them); device time per cycle from just before tc_cycle to the end of both copy streams' work, and its
+    fraction of the per-step link bound (a drained cycle pays its own up/off imbalance, which the bound includes)."""
+    tot_ms, moved, bound_s = 0.0, 0, 0.0
     for _ in range(n):
         flush.zero_()
         torch.cuda.synchronize(dev)
@@ -764,8 +770,12 @@ def per_cycle_drain(torch, dev, cycle, ups, offs, B, n, flush):
         tot_ms += max(ev["startu"].elapsed_time(ev["endu"]), ev["startu"].elapsed_time(ev["endo"]),
                       ev["starto"].elapsed_time(ev["endu"]), ev["starto"].elapsed_time(ev["endo"]))
         moved += (nu + no) * B
+        if link:
+            bound_s += step_link_bound_s(nu * B, no * B, link)
     return {"value": moved / (tot_ms * 1e-3) / 1e9 if tot_ms else None, "unit": "GB/s", "cycles": n,
-            "how": "tc_cycle + tc_sync per cycle (drained), L2 flushed between cycles"}
+            "link_frac": bound_s * 1e3 / tot_ms if (link and tot_ms) else None,
+            "how": "tc_cycle + tc_sync per cycle (drained), L2 flushed between cycles; link_frac = sum of the "
+                   "per-step link bounds / the measured time"}
 
 
 def host_enqueue_summary(recs, step_ms):

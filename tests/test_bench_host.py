@@ -137,3 +137,13 @@ def test_oracle_host_sample_fits(name, G):
     import numpy as np
     sizes = agent_sizes(small, np.random.default_rng(small.seed))
     assert sum(sizes) <= 0.6 * small.N + len(sizes)
+
+
+def test_step_link_bound():
+    """Per drained step: the smaller direction at half the bidirectional peak, the excess at the larger direction's
+    unidirectional peak."""
+    link = {"h2d_gbs": 50.0, "d2h_gbs": 40.0, "bidir_gbs": 80.0}
+    assert bench.step_link_bound_s(40e9, 40e9, link) == pytest.approx(1.0)
+    assert bench.step_link_bound_s(100e9, 0.0, link) == pytest.approx(2.0)          # H2D alone at 50
+    assert bench.step_link_bound_s(0.0, 80e9, link) == pytest.approx(2.0)           # D2H alone at 40
+    assert bench.step_link_bound_s(90e9, 40e9, link) == pytest.approx(1.0 + 1.0)    # 40 both ways + 50 H2D
