@@ -20,6 +20,10 @@ RUNS = [  # (name, L, H, D, N, S, d2h, h2d, variant, staging, peer)
     ("c2ish-direct-v0", 4, 4, 128, 40, 16, tcb.XFER_DIRECT, tcb.XFER_DIRECT, 0, 0, 0),
     ("c2ish-direct-v1", 4, 4, 128, 40, 16, tcb.XFER_DIRECT, tcb.XFER_DIRECT, 1, 0, 0),
     ("c2ish-direct-v2", 4, 4, 128, 40, 16, tcb.XFER_DIRECT, tcb.XFER_DIRECT, 2, 0, 0),
+    ("c2ish-direct-default", 4, 4, 128, 40, 16, tcb.XFER_DIRECT, tcb.XFER_DIRECT, None, 0, 0),
+    ("c2ish-direct-v4", 4, 4, 128, 40, 16, tcb.XFER_DIRECT, tcb.XFER_DIRECT, 4, 0, 0),
+    ("c2ish-staged-v4", 4, 4, 128, 40, 16, tcb.XFER_STAGED, tcb.XFER_STAGED, 4, 0, 0),
+    ("c2ish-staged-2blocks", 4, 4, 128, 40, 16, tcb.XFER_STAGED, tcb.XFER_STAGED, None, 1, 0),
     ("c2ish-copy", 4, 4, 128, 40, 16, tcb.XFER_COPY, tcb.XFER_COPY, None, 0, 0),
     ("c2ish-peer", 4, 4, 128, 40, 16, tcb.XFER_STAGED, tcb.XFER_STAGED, None, 0, 8),
 ]
@@ -38,7 +42,8 @@ def main():
         p.fill(3)
         r = Replayer(p)
         ops = c1_worked_example() if name.startswith("c1") else []
-        ops += fuzz_script(11, n_ops=60, n_agents=3, n_classes=2, N=N, max_alloc=6, gradual=True)
+        ops += fuzz_script(11, n_ops=60, n_agents=3, n_classes=2, N=N, max_alloc=6, gradual=True, retire=True,
+                           lags=(1, 2, 3))
         tr = r.run(ops)
         p.sync()
         ids = np.arange(min(8, N), dtype=np.int32)
