@@ -393,7 +393,8 @@ def run_ours(args):
     gen = CycleGen(cfg, agents, combined=True)
     handles, sizes = {}, {}
 
-    drains = [0]
+    drains = [0]                               # refused cycles retried after a tc_sync
+    ladders = [0]                              # refused cycles retried after a tc_retire (then maybe the sync)
     lag = [1]
 
     def cycle(record=None, retire="sync"):
@@ -420,10 +421,17 @@ def run_ours(args):
                     _, out_h = pool.cycle_arrays(hs, uoff, ags, ooff, ids)
                 except tcb.TcError as e:            # refused, nothing changed (host buffer / blocks held by the
                     if e.status not in (tcb.E_NOHOST, tcb.E_NOBLOCKS) or retire == "sync":   # undrained cycles):
-                        raise                                                              # drain and retry once
-                    pool.sync()
-                    drains[0] += 1
-                    _, out_h = pool.cycle_arrays(hs, uoff, ags, ooff, ids)
+                        raise                       # retire the previous cycle's transfers and retry, then drain
+                    pool.retire(1)
+                    ladders[0] += 1
+                    try:
+                        _, out_h = pool.cycle_arrays(hs, uoff, ags, ooff, ids)
+                    except tcb.TcError as e2:
+                        if e2.status not in (tcb.E_NOHOST, tcb.E_NOBLOCKS):
+                            raise
+                        pool.sync()
+                        drains[0] += 1
+                        _, out_h = pool.cycle_arrays(hs, uoff, ags, ooff, ids)
                 for a, h, t in zip(ags, out_h, tabs):
                     handles[int(a)] = int(h)
                     sizes[int(h)] = len(t)
@@ -480,7 +488,7 @@ def run_ours(args):
         e1 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         for e, st in zip(e0, (ups, offs_)):
             e.record(st)
-        drains[0] = 0
+        drains[0] = ladders[0] = 0
         for k in range(args.steps):
             th = time.perf_counter()
             nu, no = cycle(retire="retire")
@@ -674,9 +682,9 @@ def run_ours(args):
                    "retire_lag": lag[0] if args.retire == "each" else None,
                    "step": (f"tc_cycle + tc_retire_lag({lag[0]}) (retire the transfers enqueued before the "
                             f"{lag[0]}-th previous point, do not drain the last {lag[0]} cycles'); "
-                            "a cycle the host buffer / free blocks refuse is retried once after a tc_sync "
-                            f"({drains[0]} of {n_steps} steps needed it); a tc_sync drains the last cycle inside the "
-                            "timed region" if args.retire == "each" else
+                            "a cycle the host buffer / free blocks refuse is retried after a tc_retire, then once "
+                            f"more after a tc_sync ({ladders[0]} of {n_steps} steps needed the retire, {drains[0]} the "
+                            "sync); a tc_sync drains the last cycle inside the timed region" if args.retire == "each" else
                             "tc_cycle + tc_sync (drain and retire every cycle)"),
                    "parallelism": f"{world} independent ranks" + (f", head-sharded G={G}" if G > 1 else ""),
                    "numa": numa,

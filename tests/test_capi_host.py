@@ -290,3 +290,35 @@ def test_config_scripts_retire_each_match_oracle(name):
     ops = ops[:n_setup] + [("retire",) if op[0] == "sync" else ("cycle_r",) + op[1:] if op[0] == "cycle" else op
                            for op in ops[n_setup:]] + [("sync",)]
     o, c = replay_both(ops, cfg.N, cfg.host_slots(), max_bpa=cfg.max_blocks_per_agent)
+
+
+@pytest.mark.parametrize("name,lag", [("c3", 2), ("c4", 1), ("c5", 1), ("c2", 4)])
+def test_retire_ladder_loop_matches_oracle(name, lag):
+    """bench.py's retire-each loop with the refusal ladder (a refused tc_cycle is retried after tc_retire, then after
+    tc_sync) at full size: identical statuses, ids, handles, tables and counters on the library and the oracle, and
+    the ladder is actually exercised for the configs whose host buffers cannot carry the lag."""
+    cfg = CONFIGS[name]
+    ops = build_script(cfg, 12, combined=True)
+    n_setup = next(i for i, op in enumerate(ops) if op[0] == "cycle")
+    rt = ("retire",) if lag == 1 else ("retire", lag)
+    ops = ops[:n_setup] + [rt if op[0] == "sync" else ("cycle_r",) + op[1:] if op[0] == "cycle" else op
+                           for op in ops[n_setup:]] + [("sync",)]
+    o = OraclePool(cfg.N, cfg.host_slots(), max_agents=1024, max_blocks_per_agent=cfg.max_blocks_per_agent,
+                   store=ProvStore(cfg.N, cfg.host_slots()))
+    c = meta_pool(cfg.N, cfg.host_slots(), max_bpa=cfg.max_blocks_per_agent)
+    calls = {"retire": 0}
+    orig = c.retire
+
+    def counting_retire(k=1):
+        calls["retire"] += 1
+        return orig(k)
+    c.retire = counting_retire
+    ro, rc = Replayer(o), Replayer(c)
+    for i, op in enumerate(ops):
+        a, b = ro.step(op), rc.step(op)
+        assert a == b, (name, i, op)
+        assert a[0] == 0, (name, i, op)
+    n_retire_ops = sum(1 for op in ops if op[0] == "retire")
+    if name in ("c3", "c4", "c5"):
+        assert calls["retire"] > n_retire_ops            # some cycles were refused and took the ladder
+    assert stats_view(o.stats()) == stats_view(c.stats())

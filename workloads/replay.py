@@ -66,7 +66,8 @@ class Replayer:
                 for a in op[1]:
                     self.handles[a].popleft()
             elif kind in ("cycle", "cycle_r"):   # ("cycle", [upload agents], [(agent, sel), ...])
-                # cycle_r: a refused cycle (no host slots / device blocks: nothing changed) is retried once after a
+                # cycle_r: a refused cycle (no host slots / device blocks: nothing changed) is retried after a
+                # tc_retire (the previous cycle's transfers return their slots / blocks), then once more after a
                 # tc_sync — the caller policy of bench.py's retire-each loop ("the caller retries")
                 items = [(a, self._ids(a, sel)) for a, sel in op[2]]       # resolved on pre-cycle tables
                 taken = defaultdict(int)
@@ -80,8 +81,14 @@ class Replayer:
                 except Exception as e:  # noqa: BLE001
                     if kind != "cycle_r" or getattr(e, "status", None) not in (-2, -3):
                         raise
-                    p.sync()
-                    news, out_h = p.cycle(hs, items)
+                    p.retire(1)
+                    try:
+                        news, out_h = p.cycle(hs, items)
+                    except Exception as e2:  # noqa: BLE001
+                        if getattr(e2, "status", None) not in (-2, -3):
+                            raise
+                        p.sync()
+                        news, out_h = p.cycle(hs, items)
                 for a in op[1]:
                     self.handles[a].popleft()
                 for (a, _), h in zip(op[2], out_h):
