@@ -56,17 +56,17 @@ def test_reference_arm_json_line():
 
 
 def test_choose_retire_lag():
-    """bench.py's retire-loop choice: drained when one extra cycle does not fit, else the deepest lag <= 4 that fits;
-    an explicit --retire-lag wins."""
+    """bench.py's retire-loop choice: retire-each at the deepest lag <= 4 that fits (1 if none: refused cycles take
+    the retire ladder); an explicit --retire / --retire-lag wins."""
     from bench import choose_retire
     # C2-like: 11.8 k free slots, 19 k free blocks, cycles of ~330 blocks -> lag 4
     assert choose_retire("auto", 0, 11796, 19000, 330, 330) == ("each", 4)
     # host buffer for exactly 1 + 2 cycles (x1.1): lag 2
     assert choose_retire("auto", 0, int(1.1 * 3 * 1000) + 1, 10 ** 6, 1000, 1000) == ("each", 2)
-    # not even one extra cycle: drained
-    assert choose_retire("auto", 0, 1500, 10 ** 6, 1000, 1000) == ("sync", 1)
+    # not even one extra cycle: still retire-each at lag 1 (refused cycles take the retire ladder)
+    assert choose_retire("auto", 0, 1500, 10 ** 6, 1000, 1000) == ("each", 1)
     # free blocks bind: up_max + 2 off_max (x1.1) = 3300 > 3000
-    assert choose_retire("auto", 0, 10 ** 6, 3000, 1000, 1000) == ("sync", 1)
+    assert choose_retire("auto", 0, 10 ** 6, 3000, 1000, 1000) == ("each", 1)
     assert choose_retire("each", 2, 0, 0, 1000, 1000) == ("each", 2)
     assert choose_retire("sync", 0, 10 ** 6, 10 ** 6, 10, 10) == ("sync", 4)
 
