@@ -141,11 +141,14 @@ tc_status tc_set_xfer_mode(tc_pool *p, int32_t d2h, int32_t h2d);
    Uses pool blocks [0, 2k) and 2k free host slots (k = probe_bytes / B, shrunk to what is free; TC_E_NOHOST if not
    even 1 + 1 fit): the gathered blocks are only read and the scattered ones receive their own bytes back, so the pool's
    contents are unchanged — but the caller must not run kernels on the pool meanwhile.  Blocking.
-   gbs[i] = 2 * probe bytes / cycle time for combination i = 2 * (d2h is STAGED) + (h2d is STAGED). */
+   gbs[i] = 2 * probe bytes / cycle time for combination i = 2 * (d2h is STAGED) + (h2d is STAGED).  Then, per
+   direction alone, batches of 1, 2, 4, ... (<= 64) blocks are timed DIRECT vs STAGED: AUTO sends batches up to the
+   largest size where DIRECT was never slower (direct_max_bytes[dir]; 0 = never) through the DIRECT kernel. */
 typedef struct tc_calibration_t {
     int32_t d2h, h2d;          /* the chosen modes (what AUTO directions now use) */
     int64_t probe_bytes;       /* bytes per direction actually probed */
     double gbs[4];
+    int64_t direct_max_bytes[2];   /* [0] offload (D2H), [1] upload (H2D): AUTO's small-batch DIRECT crossover */
 } tc_calibration_t;
 tc_status tc_calibrate(tc_pool *p, int64_t probe_bytes, tc_calibration_t *out);
 /* Launch configuration of one kernel path: path 0 = direct D2H gather, 1 = direct H2D scatter, 2 = device-side

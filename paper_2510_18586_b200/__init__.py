@@ -68,7 +68,7 @@ class Timing(ctypes.Structure):
 
 class Calibration(ctypes.Structure):
     _fields_ = [("d2h", ctypes.c_int32), ("h2d", ctypes.c_int32), ("probe_bytes", ctypes.c_int64),
-                ("gbs", ctypes.c_double * 4)]
+                ("gbs", ctypes.c_double * 4), ("direct_max_bytes", ctypes.c_int64 * 2)]
 
 
 class TraceRec(ctypes.Structure):
@@ -473,7 +473,8 @@ class Pool:
         names = {XFER_DIRECT: "direct", XFER_STAGED: "staged"}
         return {"d2h": names[c.d2h], "h2d": names[c.h2d], "probe_bytes": c.probe_bytes,
                 "gbs": {f"{a}/{b}": c.gbs[2 * i + j] for i, a in enumerate(("direct", "staged"))
-                        for j, b in enumerate(("direct", "staged"))}}
+                        for j, b in enumerate(("direct", "staged"))},
+                "direct_max_bytes": {"d2h": int(c.direct_max_bytes[0]), "h2d": int(c.direct_max_bytes[1])}}
 
     def set_launch_config(self, path: int, ctas: int = 0, threads: int = 256, variant: int = 0):
         """path 0 = direct D2H, 1 = direct H2D, 2 = device-side (staged/device tier); variant 1 = TMA bulk."""

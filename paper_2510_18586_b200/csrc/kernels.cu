@@ -387,9 +387,12 @@ cudaError_t launch_cap(bool gather, const XferDesc *host_desc, int32_t n, const 
     if (variant == 1 || variant == 3) {
         // ring bytes per CTA: 128 KiB, one CTA per SM (1) / 96 KiB, two resident per SM (3).  stages = ring / piece,
         // so small chunks (C5's 4 KiB) keep as many bytes in flight as large ones.  Variant 3's default grid follows
-        // the launch size: ~128 KiB per CTA, between 3 and 15 CTAs per SM — several waves of short CTAs let the block
-        // scheduler even out per-channel speed differences, while a small launch keeps enough work per CTA to fill
-        // its ring (profiles/r01_tier_probe_grid_v4.log: 0.95-1.0 of the HBM copy peak from 100 MiB up, C2 and C5).
+        // the launch size: ~128 KiB per CTA, between 2 and 15 CTAs per SM — several waves of short CTAs let the block
+        // scheduler even out per-channel speed differences (profiles/r01_tier_probe_grid_v4.log: 0.95-1.0 of the HBM
+        // copy peak from 100 MiB up, C2 and C5); up to 4 waves the grid is rounded to whole waves of 296 CTAs (two per
+        // SM), so a launch never ends on a partial wave: 32 MiB runs as one wave instead of 1.5 waves of 444 (0.88-0.92
+        // vs 0.81-0.84 of the copy peak), 4-16 MiB up to 30 % shorter, 47 MiB without its 1.3-wave tail
+        // (profiles/r02_tier_probe_c{2,5}_*.json).
         const int32_t piece = (int32_t)std::min<int64_t>(g.chunk, kPieceMax);
         const int64_t K = (int64_t)n * g.two_l * ((g.chunk + piece - 1) / piece);
         const int64_t ring = tma_ring_override() > 0 ? tma_ring_override() : (variant == 1 ? 128 << 10 : 96 << 10);
@@ -397,7 +400,14 @@ cudaError_t launch_cap(bool gather, const XferDesc *host_desc, int32_t n, const 
         int64_t want = ctas;
         if (want <= 0) {
             const int64_t bytes = (int64_t)n * g.two_l * g.chunk;
-            want = variant == 1 ? 148 : std::max<int64_t>(444, std::min<int64_t>(2220, bytes >> 17));
+            want = bytes >> 17;                      // ~128 KiB per CTA
+            if (variant == 1) {
+                want = 148;
+            } else if (want <= 1184) {               // up to 4 waves: whole waves of 296 (2 per SM), no partial one
+                want = std::max<int64_t>(1, (want + 148) / 296) * 296;
+            } else {
+                want = std::min<int64_t>(2220, want);
+            }
         }
         split(K, want, 1, &grid, &per);
         const size_t smem = (size_t)stages * piece + stages * sizeof(uint64_t);

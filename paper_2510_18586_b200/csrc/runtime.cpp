@@ -319,7 +319,7 @@ tc_status Pool::create(const tc_pool_desc &d) {
     auto_choice[1] = env_int("TC_AUTO_H2D", TC_XFER_STAGED);
     if (auto_dir[0]) mode_d2h = auto_mode(0);
     if (auto_dir[1]) mode_h2d = auto_mode(1);
-    auto_direct_bytes = env_int("TC_AUTO_DIRECT_KIB", 2048) * 1024ll;
+    auto_direct_bytes[0] = auto_direct_bytes[1] = env_int("TC_AUTO_DIRECT_KIB", 2048) * 1024ll;
     // completion events, created up front (a deep retire lag keeps dozens in flight; no driver call inside a loop)
     for (int i = 0; i < 256; ++i) {
         cudaEvent_t e;
@@ -523,7 +523,8 @@ tc_status Pool::xfer_init(XferJob &j, bool gather, int32_t mode, const std::vect
     j.slot_of = slot_of;
     j.s = s;
     j.n = (int64_t)desc->size();
-    if (j.mode == TC_XFER_STAGED && auto_dir[gather ? 0 : 1] && j.n * B <= auto_direct_bytes) j.mode = TC_XFER_DIRECT;
+    if (j.mode == TC_XFER_STAGED && auto_dir[gather ? 0 : 1] && j.n * B <= auto_direct_bytes[gather ? 0 : 1])
+        j.mode = TC_XFER_DIRECT;
     if (j.mode != TC_XFER_STAGED || j.n == 0) return TC_OK;
     const int dir = gather ? 0 : 1;
     if (!staging[dir]) TC_CUDA(cudaMalloc(&staging[dir], staging_bytes), "staging alloc");
@@ -576,9 +577,61 @@ tc_status Pool::xfer_init(XferJob &j, bool gather, int32_t mode, const std::vect
 }
 
 // AUTO: the path measured fastest for a full scheduling cycle on B200 (both directions concurrently).
-// A batch of at most auto_direct_bytes still takes the DIRECT kernel: one launch instead of kernel + DMA, ~5 µs
-// sooner for 1-2 blocks and equal from ~2 MiB up (profiles/r01_sweep_c{2,5}.json).
+// A batch of at most auto_direct_bytes[dir] still takes the DIRECT kernel: one launch instead of kernel + DMA, ~5 µs
+// sooner for 1-2 blocks and equal from ~2 MiB up (profiles/r01_sweep_c{2,5}.json); tc_calibrate re-measures the
+// crossover per direction on the box (calibrate_small).
 int32_t Pool::auto_mode(int dir) const { return auto_choice[dir]; }
+
+// The small-batch crossover (north_star: DIRECT "chosen against a device-staging path ... according to the measured
+// bandwidth"): one direction alone, batches of 1, 2, 4, ... blocks, DIRECT vs STAGED completion time (best of 5 after
+// a warm-up); auto_direct_bytes[dir] = the largest size up to which DIRECT was never slower.  Same blocks and slots as
+// calibrate's probe, so the pool's contents stay unchanged (gathers only read; scatters rewrite B's own bytes).
+tc_status Pool::calibrate_small(int64_t k, const std::vector<XferDesc> &da, const std::vector<XferDesc> &db,
+                                const std::vector<int64_t> &sa, const std::vector<int64_t> &sb, tc_calibration_t *out) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+        if (e0) cudaEventDestroy(e0);
+        return cuda_fail(cudaErrorMemoryAllocation, "calibrate events");
+    }
+    tc_status st = TC_OK;
+    for (int dir = 0; dir < 2 && st == TC_OK; ++dir) {
+        const bool gather = dir == 0;
+        cudaStream_t s = gather ? s_off : s_up;
+        int64_t best_ok = 0;
+        bool still = true;
+        for (int64_t m = 1; m <= std::min<int64_t>(k, 64) && st == TC_OK; m *= 2) {
+            std::vector<XferDesc> d(gather ? da.begin() : db.begin(), (gather ? da.begin() : db.begin()) + m);
+            std::vector<int64_t> sl(gather ? sa.begin() : sb.begin(), (gather ? sa.begin() : sb.begin()) + m);
+            double t[2] = {1e30, 1e30};
+            for (int rep = 0; rep < 6 && st == TC_OK; ++rep) {
+                for (int c = 0; c < 2 && st == TC_OK; ++c) {
+                    if (cudaStreamSynchronize(s) != cudaSuccess || cudaEventRecord(e0, s) != cudaSuccess) {
+                        st = cuda_fail(cudaGetLastError(), "calibrate small");
+                        break;
+                    }
+                    if ((st = enqueue_xfer(gather, c == 0 ? TC_XFER_DIRECT : TC_XFER_STAGED, d, sl, s)) != TC_OK) break;
+                    float ms = 0.f;
+                    if (cudaEventRecord(e1, s) != cudaSuccess || cudaEventSynchronize(e1) != cudaSuccess ||
+                        cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess) {
+                        st = cuda_fail(cudaGetLastError(), "calibrate small timing");
+                        break;
+                    }
+                    if (rep > 0) t[c] = std::min(t[c], (double)ms);
+                }
+            }
+            if (st != TC_OK) break;
+            if (still && t[0] <= t[1]) best_ok = m * B;
+            else still = false;
+        }
+        if (st == TC_OK) {
+            auto_direct_bytes[dir] = best_ok;
+            out->direct_max_bytes[dir] = best_ok;
+        }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return st;
+}
 
 tc_status Pool::calibrate(int64_t probe_bytes, tc_calibration_t *out) {
     if (meta_only) return TC_E_NODEV;
@@ -634,6 +687,7 @@ tc_status Pool::calibrate(int64_t probe_bytes, tc_calibration_t *out) {
     }
     for (cudaEvent_t e : {e0, e1, e2})
         if (e) cudaEventDestroy(e);
+    if (st == TC_OK) st = calibrate_small(k, da, db, sa, sb, out);
     auto_dir[0] = saved_auto[0];
     auto_dir[1] = saved_auto[1];
     if (st != TC_OK) return st;

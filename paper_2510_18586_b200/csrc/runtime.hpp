@@ -137,7 +137,9 @@ struct Pool {
     bool auto_dir[2] = {false, false};        // the direction's mode came from AUTO (small batches go DIRECT)
     int32_t auto_choice[2] = {TC_XFER_STAGED, TC_XFER_STAGED};   // what AUTO resolves to (tc_calibrate)
     tc_status calibrate(int64_t probe_bytes, tc_calibration_t *out);
-    int64_t auto_direct_bytes = 2ll << 20;
+    tc_status calibrate_small(int64_t k, const std::vector<XferDesc> &da, const std::vector<XferDesc> &db,
+                              const std::vector<int64_t> &sa, const std::vector<int64_t> &sb, tc_calibration_t *out);
+    int64_t auto_direct_bytes[2] = {2ll << 20, 2ll << 20};   // per direction: AUTO batches up to this go DIRECT
     // launch config per path: [0] direct D2H, [1] direct H2D, [2] device tier + staged kernels, [3] peer tier
     int ctas[4] = {0, 0, 0, 0}, nthreads[4] = {256, 256, 256, 256}, variant[4] = {0, 0, 3, 3};
 

@@ -360,6 +360,9 @@ def test_calibrate_keeps_pool_and_sets_auto():
     before = c.stats()
     cal = c.calibrate(8 << 20)
     assert cal["probe_bytes"] > 0 and all(v > 0 for v in cal["gbs"].values())
+    # the measured small-batch crossover: a whole number of blocks (0 = DIRECT never faster), at most 64 blocks
+    for v in cal["direct_max_bytes"].values():
+        assert v % c.block_bytes == 0 and 0 <= v <= 64 * c.block_bytes
     assert np.array_equal(c.kv_tensor().cpu().numpy(), pool0)
     after = c.stats()
     assert {k: before[k] for k in ("free", "alloc", "host_free", "host_used")} == \
