@@ -647,6 +647,14 @@ def run_ours(args):
                 "share_of_kernel_time": kd["ms_total"] / sum(v["ms_total"] for v in kern_only.values())}
         if "peer" not in dom:
             roof.update(ncu_traffic(cfg.name, "gather" if dom.startswith("offload") else "scatter", kd))
+        # cross-check with CUDA events recorded on the launching stream around each launch of the same kernel (the
+        # diagnostic steps after the timed region, timing mode 1; includes the launch's own start-up on the stream)
+        ems, ecnt, ebytes = diag.get(dom, (0.0, 0, 0))
+        if ecnt and ems:
+            scale = 2 if kd["bound"] == "hbm" else 1           # HBM kernels count read + write, as above
+            roof["event_check"] = {"ms_per_launch": ems / ecnt, "achieved": scale * ebytes / (ems * 1e-3) / 1e9,
+                                   "launches": ecnt, "how": "CUDA events on the kernel's own stream around every "
+                                   f"launch of the {n_diag} diagnostic steps (timing mode 1)"}
     # the step's binding resource is the host link: per-direction DMA/kernel rate and a per-step link roofline
     link_roof = None
     if link and not args.peer:
