@@ -278,8 +278,9 @@ typedef struct tc_timing_t {
     int64_t kernel_bytes[TC_NKINDS];
 } tc_timing_t;
 /* enable: 0 off (the default: zero overhead); 1 event spans around every kernel / memcpy run plus the kernels' own
-   start/end timestamps; 2 the kernels' timestamps only (no events: does not perturb the stream schedule).  Other
-   values -> TC_E_INVAL.  If out != NULL it receives the totals accumulated since the previous call, which are then
+   start/end timestamps; 2 the kernels' timestamps only (no events: does not perturb the stream schedule); 3 event
+   spans around kernel launches only (CUDA events on the launching stream) plus the timestamps.  Other values ->
+   TC_E_INVAL.  If out != NULL it receives the totals accumulated since the previous call, which are then
    reset. */
 tc_status tc_timing(tc_pool *p, int32_t enable, tc_timing_t *out);
 /* Per-span timeline (needs tc_timing enabled): kind as in tc_timing_t, start/end in ms relative to the first span

@@ -428,7 +428,7 @@ tc_status tc_stats(tc_pool *p, tc_stats_t *s) {
 
 tc_status tc_timing(tc_pool *p, int32_t enable, tc_timing_t *out) {
     TC_GUARD(p) {
-        if (enable < 0 || enable > 2) return TC_E_INVAL;
+        if (enable < 0 || enable > 3) return TC_E_INVAL;
         if (!P.meta_only && (!P.kts_meta.empty() || !P.spans.empty())) {   // collected lazily (runtime.cpp)
             for (cudaStream_t s : {P.s_up, P.s_off, P.s_up_k, P.s_off_k})
                 if (cudaStreamSynchronize(s) != cudaSuccess) return P.cuda_fail(cudaGetLastError(), "timing sync");
@@ -438,6 +438,14 @@ tc_status tc_timing(tc_pool *p, int32_t enable, tc_timing_t *out) {
         }
         P.timing = P.meta_only ? 0 : enable;
         if (P.timing) P.kts_ensure();                   // allocate now, not at the first timed launch
+        if (P.timing == 1 || P.timing == 3) {           // span events created now, not inside a timed loop
+            while (P.tev_free.size() < 1024) {
+                cudaEvent_t e = nullptr;
+                if (cudaEventCreate(&e) != cudaSuccess) return P.cuda_fail(cudaGetLastError(), "timing events");
+                P.tev_free.push_back(e);
+            }
+            P.spans.reserve(512);
+        }
         if (out) {
             *out = P.tacc;
             P.tacc = tc_timing_t{};

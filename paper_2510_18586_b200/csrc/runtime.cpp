@@ -357,9 +357,13 @@ cudaEvent_t Pool::tev_get() {
     return e;
 }
 
-tc_status Pool::span_begin(cudaStream_t s, cudaEvent_t *a) {
+// Event spans: timing 1 around every kernel launch and DMA run; timing 3 around kernel launches only (the DMAs keep
+// their schedule untouched; the kernels are also stamped, as in 2).
+bool Pool::span_on(bool kernel) const { return timing == 1 || (timing == 3 && kernel); }
+
+tc_status Pool::span_begin(cudaStream_t s, cudaEvent_t *a, bool kernel) {
     *a = nullptr;
-    if (timing != 1) return TC_OK;
+    if (!span_on(kernel)) return TC_OK;
     *a = tev_get();
     if (!*a) return cuda_fail(cudaErrorMemoryAllocation, "timing event");
     TC_CUDA(cudaEventRecord(*a, s), "timing event");
@@ -367,7 +371,7 @@ tc_status Pool::span_begin(cudaStream_t s, cudaEvent_t *a) {
 }
 
 tc_status Pool::span_end(cudaStream_t s, int32_t kind, cudaEvent_t a, int64_t bytes, bool link) {
-    if (timing != 1 || !a) return TC_OK;
+    if (!a) return TC_OK;
     cudaEvent_t b = tev_get();
     if (!b) return cuda_fail(cudaErrorMemoryAllocation, "timing event");
     TC_CUDA(cudaEventRecord(b, s), "timing event");
@@ -716,7 +720,7 @@ tc_status Pool::xfer_copy2d(XferJob &j) {
         TC_CUDA(launch_table(true, j.desc->data(), j.n, table_dev, j.s), "table kernel");
         n_launch += table_launches;
     }
-    if ((st = span_begin(j.s, &t0)) != TC_OK) return st;
+    if ((st = span_begin(j.s, &t0, /*kernel=*/false)) != TC_OK) return st;
     for (int64_t i = 0; i < j.n; ++i) {
         char *pool_p = kv + (int64_t)(*j.desc)[i].blk * C;
         char *host_p = host_ptr(slot_of[i]);
@@ -757,7 +761,7 @@ tc_status Pool::xfer_copy(XferJob &j, int64_t a, int64_t b, char *base) {
     const bool to_host = j.gather;
     const auto &slot_of = *j.slot_of;
     cudaEvent_t t0;
-    tc_status s0 = span_begin(j.s, &t0);
+    tc_status s0 = span_begin(j.s, &t0, /*kernel=*/false);
     if (s0 != TC_OK) return s0;
     cp_dst.clear(); cp_src.clear(); cp_size.clear();
     for (int64_t i = a; i < b;) {

@@ -169,12 +169,13 @@ struct Pool {
         int64_t bytes;
         bool link;                           // host-link side of a transfer (DMA or direct kernel)
     };
-    int32_t timing = 0;                      // 0 off, 1 event spans + kernel timestamps, 2 kernel timestamps
+    int32_t timing = 0;   // 0 off, 1 event spans + kernel timestamps, 2 kernel timestamps, 3 kernel spans + timestamps
     std::vector<Span> spans;
     std::vector<cudaEvent_t> tev_free;
     tc_timing_t tacc{};
     cudaEvent_t tev_get();
-    tc_status span_begin(cudaStream_t s, cudaEvent_t *a);
+    tc_status span_begin(cudaStream_t s, cudaEvent_t *a, bool kernel = true);
+    bool span_on(bool kernel) const;
     tc_status span_end(cudaStream_t s, int32_t kind, cudaEvent_t a, int64_t bytes, bool link = true);
     void spans_collect();
     bool check = false;                      // TC_CHECK=1: invariants after every mutating call
