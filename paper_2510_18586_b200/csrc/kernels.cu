@@ -412,8 +412,17 @@ cudaError_t launch_cap(bool gather, const XferDesc *host_desc, int32_t n, const 
         split(K, want, 1, &grid, &per);
         const size_t smem = (size_t)stages * piece + stages * sizeof(uint64_t);
         auto fn = gather ? k_xfer_bulk<true, kCap> : k_xfer_bulk<false, kCap>;
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
+        // the opt-in dynamic shared memory is raised once per kernel (and device) to the largest size seen: a
+        // cudaFuncSetAttribute on every launch sat on the host's launch path (tens of µs per launch)
+        static size_t smem_set[2][64] = {};
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+        size_t &done = smem_set[gather ? 1 : 0][dev];
+        if (smem > done) {
+            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            done = smem;
+        }
         fn<<<(unsigned)grid, 32, smem, s>>>(dd, n, g, kv, table, per, piece, stages);
         return cudaGetLastError();
     }
