@@ -205,18 +205,27 @@ def hostlink_peak(torch, dev, nbytes=1 << 30, reps=10):
             b = max(b, nb / (e0.elapsed_time(e1) * 1e-3) / 1e9)
         return b
 
+    split = {"h2d": 0.0, "d2h": 0.0}
+
     def bidir():
         cur = torch.cuda.current_stream(dev)
         s1.wait_stream(cur); s2.wait_stream(cur)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record(s1); ev[2].record(s2)
         with torch.cuda.stream(s1):
             d.copy_(h, non_blocking=True)
         with torch.cuda.stream(s2):
             h2.copy_(d2, non_blocking=True)
+        ev[1].record(s1); ev[3].record(s2)
         cur.wait_stream(s1); cur.wait_stream(s2)
+        ev[3].synchronize(); ev[1].synchronize()
+        split["h2d"] = max(split["h2d"], nbytes / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9)
+        split["d2h"] = max(split["d2h"], nbytes / (ev[2].elapsed_time(ev[3]) * 1e-3) / 1e9)
 
     r = {"h2d_gbs": best(lambda: d.copy_(h, non_blocking=True), nbytes),
          "d2h_gbs": best(lambda: h.copy_(d, non_blocking=True), nbytes),
          "bidir_gbs": best(bidir, 2 * nbytes), "bytes": nbytes, "how": "torch pinned copy_ 1 GiB, best of 10"}
+    r["bidir_split_gbs"] = dict(split)          # each direction's own rate inside the concurrent pair (best)
     del h, h2, d, d2
     return r
 
