@@ -558,11 +558,14 @@ def run_ours(args):
     pool.timing(1)
     pool.timing(1)
     pool.timeline_arm(200000)
-    pool.trace(100000)                         # per-call records: host enqueue cost of rows a2 / a5 (and --trace)
     n_diag = min(args.steps, int(os.environ.get("TC_DIAG_STEPS", 20)))
     # TC_DIAG_RETIRE=1: run the diagnostic cycles in the timed loop's retire-each form (one timeline over all of
     # them, for TC_DUMP_TIMELINE / tools/timeline_gaps.py) instead of drained
     diag_each = args.retire == "each" and os.environ.get("TC_DIAG_RETIRE") == "1"
+    # per-call records (host enqueue cost of rows a2 / a5, and --trace): each record's completion stamp is a host
+    # callback queued on the copy stream, which holds the stream's next DMA until the host runs it — so not in a
+    # retire-each timeline (it would show gaps the timed loop does not have)
+    pool.trace(0 if diag_each else 100000)
     for _ in range(n_diag):
         cycle(retire="retire" if diag_each else "sync")
     if diag_each:
