@@ -27,6 +27,6 @@ PY
 if [ -n "$NCU" ]; then
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 20000 --csv --log-file gpurun_out/launches_default_cmd_$V.csv \
    python3 bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/ncu_launch_default_$V.log 2>&1; echo "ncu launch list rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_xfer_bulk -s 40 -c 2 -o gpurun_out/prof_c3_loop_$V -f \
-   python3 bench.py --steps 6 --warmup 3 --quick --no-cpu-baseline > gpurun_out/ncu_full_loop_$V.log 2>&1; echo "ncu full rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_xfer_bulk -s 60 -c 2 -o gpurun_out/prof_c3_loop_$V -f \
+   python3 bench.py --steps 6 --warmup 3 --quick --no-cpu-baseline --mode staged > gpurun_out/ncu_full_loop_$V.log 2>&1; echo "ncu full rc=$?"
 fi
