@@ -147,3 +147,19 @@ def test_step_link_bound():
     assert bench.step_link_bound_s(100e9, 0.0, link) == pytest.approx(2.0)          # H2D alone at 50
     assert bench.step_link_bound_s(0.0, 80e9, link) == pytest.approx(2.0)           # D2H alone at 40
     assert bench.step_link_bound_s(90e9, 40e9, link) == pytest.approx(1.0 + 1.0)    # 40 both ways + 50 H2D
+
+
+def test_offload_size_sweep_logic_on_metadata_pool():
+    """bench.py's C5 sweep (both directions per tc_cycle, roles swapping each rep) drives a metadata-only pool to
+    completion: one row per size, and afterwards no live handle, no pending block and both sweep agents freed."""
+    import paper_2510_18586_b200 as tcb
+    from workloads.configs import CONFIGS
+    cfg = CONFIGS["c5"]
+    p = tcb.Pool(cfg.L, cfg.H, cfg.D, cfg.T, cfg.dtype, 256, device=-1, shard_world=cfg.G, host_slots=64,
+                 max_agents=1024, max_blocks_per_agent=64)
+    before = p.stats()
+    out = bench.offload_size_sweep(p, cfg, p.block_bytes, sizes=(1, 2, 8), reps=2)
+    assert [r["blocks"] for r in out["rows"]] == [1, 2, 8]
+    s = p.stats()
+    assert s["live_handles"] == 0 and s["pending"] == 0 and s["alloc"] == before["alloc"]
+    assert s["free"] == before["free"] and s["host_free"] == before["host_free"]
