@@ -20,6 +20,7 @@
 // Work is split over CTAs at piece/tile granularity (variants 1-3), so a small launch (the staged head/tail piece)
 // still reaches every SM and a large one has no chunk-granular tail.
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -413,15 +414,18 @@ cudaError_t launch_cap(bool gather, const XferDesc *host_desc, int32_t n, const 
         const size_t smem = (size_t)stages * piece + stages * sizeof(uint64_t);
         auto fn = gather ? k_xfer_bulk<true, kCap> : k_xfer_bulk<false, kCap>;
         // the opt-in dynamic shared memory is raised once per kernel (and device) to the largest size seen: a
-        // cudaFuncSetAttribute on every launch sat on the host's launch path (tens of µs per launch)
-        static size_t smem_set[2][64] = {};
+        // cudaFuncSetAttribute on every launch sat on the host's launch path (tens of µs per launch).  Atomic: pools
+        // on several host threads may launch at once; a racing raise just sets the attribute twice (idempotent).
+        static std::atomic<size_t> smem_set[2][64] = {};
         int dev = 0;
         if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-        size_t &done = smem_set[gather ? 1 : 0][dev];
-        if (smem > done) {
+        std::atomic<size_t> &done = smem_set[gather ? 1 : 0][dev];
+        size_t seen = done.load(std::memory_order_acquire);
+        if (smem > seen) {
             cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
-            done = smem;
+            while (seen < smem && !done.compare_exchange_weak(seen, smem, std::memory_order_acq_rel)) {
+            }
         }
         fn<<<(unsigned)grid, 32, smem, s>>>(dd, n, g, kv, table, per, piece, stages);
         return cudaGetLastError();
