@@ -72,6 +72,10 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--quick", action="store_true", help="skip host-link probe and device-tier microbench")
     ap.add_argument("--no-sweep", action="store_true", help="c5: skip the 1-512 blocks-per-offload sweep")
+    ap.add_argument("--head-shards", type=int, default=0,
+                    help="c4 on one GPU: run one rank's shard of a G-GPU head-sharded run (G = 1, 2, 4, 8) — the work "
+                         "each GPU of that run does, alone on this GPU and its own host link (per-GPU flatness)")
+    ap.add_argument("--shard-rank", type=int, default=0, help="with --head-shards: which rank's shard (0 .. G-1)")
     ap.add_argument("--dry-run", action="store_true",
                     help="launcher / rendezvous / workload-plan check without a GPU: every rank joins the process group "
                          "(gloo), rank 0 prints the plan line (n_gpus, head shards, per-rank rows, cpu_baseline)")
@@ -112,6 +116,15 @@ def default_workload(world: int) -> str:
     return "c3" if world == 1 else "c4"
 
 
+def shard_rank_for(args, rank, G):
+    """This rank's head shard: rank mod G, or --shard-rank when one GPU runs one shard of a G-GPU run."""
+    if getattr(args, "head_shards", 0):
+        if not 0 <= args.shard_rank < G:
+            raise SystemExit(f"--shard-rank must be in [0, {G})")
+        return args.shard_rank
+    return rank % G if G > 1 else 0
+
+
 def workload_for(args, world):
     """(config, head shards G, scaling).  C4 is head-sharded over the ranks present (G = N: strong scaling; at N = 1
     the whole 128 GiB pool sits on one GPU).  C5 is defined on 8 x B200 (BASELINE configs[4]): G = 8 always, and N < 8
@@ -119,6 +132,11 @@ def workload_for(args, world):
     rank, independent agent sets (weak)."""
     name = args.workload or default_workload(world)
     cfg = CONFIGS[name]
+    hs = getattr(args, "head_shards", 0) or 0
+    if hs:
+        if name != "c4" or world != 1 or cfg.H % hs:
+            raise SystemExit("--head-shards: c4 on one GPU (N = 1), G dividing its 8 KV heads")
+        return cfg, hs, ("strong" if hs > 1 else "weak")
     if name == "c4":
         return cfg, world, ("strong" if world > 1 else "weak")
     if name == "c5":
@@ -364,7 +382,7 @@ def run_ours(args):
         else:
             dist.init_process_group(backend)
     cfg, G, scaling = workload_for(args, world)
-    shard_rank = rank % G if G > 1 else 0
+    shard_rank = shard_rank_for(args, rank, G)
     mode_d2h, mode_h2d = {"auto": (tcb.XFER_AUTO,) * 2, "direct": (tcb.XFER_DIRECT,) * 2,
                           "staged": (tcb.XFER_STAGED,) * 2, "copy": (tcb.XFER_COPY,) * 2,
                           "mixed": (tcb.XFER_DIRECT, tcb.XFER_STAGED),
@@ -711,7 +729,10 @@ def run_ours(args):
                             f"more after a tc_sync ({ladders[0]} of {n_steps} steps needed the retire, {drains[0]} the "
                             "sync); a tc_sync drains the last cycle inside the timed region" if args.retire == "each" else
                             "tc_cycle + tc_sync (drain and retire every cycle)"),
-                   "parallelism": f"{world} independent ranks" + (f", head-sharded G={G}" if G > 1 else ""),
+                   "parallelism": (f"one GPU running rank {shard_rank}'s shard of a {G}-GPU head-sharded run "
+                                   "(its own host link; the per-GPU work of that run)" if args.head_shards else
+                                   f"{world} independent ranks" + (f", head-sharded G={G}" if G > 1 else "")),
+                   "shard_rank": shard_rank,
                    "numa": numa,
                    "offload_tier": ("peer slots on GPU %d (%s) first, then host" % (
                        peer_dev, "this GPU's own HBM" if peer_dev == local else "NVLink neighbour")) if args.peer
@@ -1006,7 +1027,7 @@ def run_dry(args):
     if world > 1:
         dist.init_process_group("gloo")
     cfg, G, scaling = workload_for(args, world)
-    shard_rank = rank % G if G > 1 else 0
+    shard_rank = shard_rank_for(args, rank, G)
     my = torch.tensor([1.0, 1.0, float(cfg.block_bytes(G)), 1.0, 0.0, 0.0], dtype=torch.float64)
     rows = [my.tolist()]
     shards = [shard_rank]

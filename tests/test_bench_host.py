@@ -21,6 +21,27 @@ def test_workload_for(name, world, G, scaling):
     assert (cfg.name, g, sc) == (name, G, scaling)
 
 
+@pytest.mark.parametrize("G,r", [(1, 0), (2, 1), (4, 3), (8, 0), (8, 7)])
+def test_head_shards_one_gpu(G, r):
+    """--head-shards G --shard-rank r: one GPU runs rank r's shard of a G-GPU C4 run (per-GPU flatness line)."""
+    a = SimpleNamespace(workload="c4", head_shards=G, shard_rank=r)
+    cfg, g, sc = bench.workload_for(a, 1)
+    assert (cfg.name, g, sc) == ("c4", G, "strong" if G > 1 else "weak")
+    assert bench.shard_rank_for(a, 0, g) == r
+    assert cfg.block_bytes(g) == cfg.block_bytes(1) // G
+
+
+@pytest.mark.parametrize("kw,world", [(dict(workload="c3", head_shards=2, shard_rank=0), 1),
+                                      (dict(workload="c4", head_shards=3, shard_rank=0), 1),
+                                      (dict(workload="c4", head_shards=2, shard_rank=0), 2),
+                                      (dict(workload="c4", head_shards=2, shard_rank=2), 1)])
+def test_head_shards_rejects(kw, world):
+    with pytest.raises(SystemExit):
+        a = SimpleNamespace(**kw)
+        cfg, g, _ = bench.workload_for(a, world)
+        bench.shard_rank_for(a, 0, g)
+
+
 def test_timeline_summary():
     spans = [(0, "memcpy_h2d", 0.0, 2.0, 10), (0, "memcpy_d2h", 0.1, 2.5, 10), (0, "offload_kernel", 0.01, 0.05, 10),
              (1, "memcpy_h2d", 0.0, 1.0, 10), (1, "memcpy_d2h", 0.3, 1.5, 10)]
