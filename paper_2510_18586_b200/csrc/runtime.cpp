@@ -787,6 +787,7 @@ tc_status Pool::xfer_copy(XferJob &j, int64_t a, int64_t b, char *base) {
 // Launches the gather/scatter of n descriptors (by value in the kernel parameters, at most kMaxInlineDesc per
 // launch) with path's launch configuration; `kind` names the timing slot (0 offload, 1 upload, 2 device tier).
 tc_status Pool::launch_descs(bool gather, int32_t kind, int path, const XferDesc *d, int64_t n, cudaStream_t s) {
+    if (check) check_descs(kind, d, n);
     for (int64_t a = 0; a < n; a += kMaxInlineDesc) {
         const int32_t m = (int32_t)std::min<int64_t>(kMaxInlineDesc, n - a);
         const XferGeom g = geom(kind, m * B);
@@ -1584,6 +1585,36 @@ void Pool::trace_calls(int32_t op, const int32_t *ags, const tc_handle *hs, cons
 
 // TC_CHECK=1 (debug): the SPEC invariants re-derived from scratch after every mutating call;
 // a violation aborts with the failing invariant.  Off by default (O(N) per call).
+void Pool::check_descs(int32_t kind, const XferDesc *d, int64_t n) const {
+    auto fail = [&](int64_t i, const char *what) {
+        std::fprintf(stderr, "tokencake descriptor check failed (launch kind %d, descriptor %lld of %lld): %s\n", kind,
+                     (long long)i, (long long)n, what);
+        std::abort();
+    };
+    auto inside = [&](uint64_t x, const char *base, int64_t bytes) {
+        const uint64_t b = reinterpret_cast<uint64_t>(base);
+        return base && x >= b && x + (uint64_t)B <= b + (uint64_t)bytes;
+    };
+    const int64_t tab_n = (int64_t)max_agents * max_bpa;
+    for (int64_t i = 0; i < n; ++i) {
+        if (d[i].blk < 0 || d[i].blk >= N) fail(i, "pool block id out of range");
+        if (d[i].tab < -1 || d[i].tab >= tab_n) fail(i, "block-table index out of range");
+        const uint64_t x = d[i].ext;
+        if (x % 16) fail(i, "block image not 16-byte aligned");
+        bool ok = true;
+        if (kind == 0 || kind == 1) {            // staged kernels: inside the direction's staging buffer
+            ok = inside(x, staging[kind], staging_bytes);
+        } else if (kind == 7 || kind == 8) {     // DIRECT kernels: a host slot of the slab or of an ablation slab
+            ok = inside(x, slots.dev, slots.count * B);
+            for (const auto &kv_ : extra)
+                ok = ok || inside(x, kv_.second.dev, kv_.second.n * B);
+        } else if (kind == 5 || kind == 6) {     // peer tier: the neighbour's slab
+            ok = inside(x, peer.dev, peer.count * B);
+        }                                        // kind 2: a caller buffer (the caller owns its extent)
+        if (!ok) fail(i, "block image outside the buffer this launch may touch");
+    }
+}
+
 void Pool::check_invariants(const char *after) const {
     auto fail = [&](const char *what) {
         std::fprintf(stderr, "tokencake invariant violated after %s: %s\n", after, what);

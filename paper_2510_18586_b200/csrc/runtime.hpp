@@ -180,6 +180,9 @@ struct Pool {
     void spans_collect();
     bool check = false;                      // TC_CHECK=1: invariants after every mutating call
     void check_invariants(const char *after) const;
+    // TC_CHECK: every descriptor of a launch addresses a pool block, a table entry and a whole block image inside the
+    // buffer its kind writes to / reads from (staging, host slab, peer slab); aborts on a violation
+    void check_descs(int32_t kind, const XferDesc *d, int64_t n) const;
     void stamps_collect();
     std::vector<tc_span_t> timeline;         // per-span records (tc_timeline), capped
     // per-call trace (tc_trace): records live in a fixed array so the completion callbacks can fill t_done in place
