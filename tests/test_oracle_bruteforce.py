@@ -3,7 +3,6 @@ oracle vs the independent set-based model in tests/brute_model.py; plus all 2^8 
 offload.  States already explored at the same remaining depth (identical oracle AND model state) are not
 re-expanded: their futures are identical by determinism, so every sequence's behaviour is still covered."""
 import copy
-import itertools
 
 import numpy as np
 import pytest

@@ -3,7 +3,6 @@ import json
 import os
 
 import numpy as np
-import pytest
 
 from oracle import (ALLOC, E_BUSY, E_HANDLE, E_INVAL, E_NOBLOCKS, E_NOHOST, FREE, PENDING, BytesStore, OracleError,
                     OraclePool, ProvStore)

@@ -7,7 +7,6 @@ import sys
 import time
 
 import numpy as np
-import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2510_18586_b200 as tcb  # noqa: E402
