@@ -201,10 +201,10 @@ tc_status Pool::create(const tc_pool_desc &d) {
     if (d.layers < 1 || d.kv_heads < 1 || d.head_dim < 1 || d.block_tokens < 1 || d.n_blocks < 1) return TC_E_INVAL;
     if (d.n_blocks > INT32_MAX - 1) return TC_E_INVAL;
     if (d.dtype != TC_FP16 && d.dtype != TC_BF16) return TC_E_INVAL;
-    const int world = d.shard_world < 1 ? 1 : d.shard_world;
-    if (d.kv_heads % world || d.shard_rank < 0 || d.shard_rank >= world) return TC_E_INVAL;
+    const int g = d.shard_world < 1 ? 1 : d.shard_world;
+    if (d.kv_heads % g || d.shard_rank < 0 || d.shard_rank >= g) return TC_E_INVAL;
     L = d.layers; H = d.kv_heads; D = d.head_dim; T = d.block_tokens; dtype = d.dtype;
-    this->world = world; rank = d.shard_rank; Hl = H / world;
+    world = g; rank = d.shard_rank; Hl = H / g;
     N = d.n_blocks;
     C = (int64_t)T * Hl * D * 2;
     if (C % 16 || (D * 2) % 8) return TC_E_INVAL;   // 16-byte vector path; 8-byte content words per head row
@@ -1650,9 +1650,9 @@ void Pool::check_invariants(const char *after) const {
         if (alloc.claimed[c] < 0) fail("negative claim");
     if (!unbuffered) {
         int64_t host_in_use = 0, peer_in_use = 0, rel_host = 0, rel_peer = 0;
-        for (const auto &kv : handles) {
-            if (kv.second.state != kOffloaded) continue;
-            for (int64_t s : kv.second.slots) (is_peer(s) ? peer_in_use : host_in_use) += 1;
+        for (const auto &hk : handles) {
+            if (hk.second.state != kOffloaded) continue;
+            for (int64_t s : hk.second.slots) (is_peer(s) ? peer_in_use : host_in_use) += 1;
         }
         for (int64_t s : slots.released) (is_peer(s) ? rel_peer : rel_host) += 1;
         if (slots.nfree + host_in_use + rel_host != slots.count) fail("host slot conservation");
