@@ -375,7 +375,9 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
-    if world > 1:
+    # TC_BENCH_DIST=1 (under torchrun): join the process group even at world size 1, so the N-rank code path — NCCL
+    # barrier, all_reduce and all_gather of device tensors — runs on a one-GPU box
+    if world > 1 or os.environ.get("TC_BENCH_DIST") == "1":
         import torch.distributed as dist
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
