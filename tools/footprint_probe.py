@@ -7,7 +7,9 @@ For a pinned slab of S GiB (cudaHostAlloc through torch pin_memory) and device b
   runs     each rep moves 1 GiB as R-MiB contiguous runs at shuffled slab offsets (the loop's DMA-run pattern)
 Each line: mode, per-direction GB/s inside the concurrent pair and the pair's total, best and median of `reps`.
 
-    python tools/footprint_probe.py [slab_GiB=16] [reps=8] [run_MiB=64]
+    python tools/footprint_probe.py [slab_GiB=16] [reps=8] [run_MiB=64] [alloc=torch|lib]
+
+alloc=lib allocates the slab as libtokencake does (cudaHostAlloc Portable | Mapped) instead of torch's pin_memory.
 """
 import json
 import random
@@ -21,9 +23,20 @@ def main():
     slab_gib = int(sys.argv[1]) if len(sys.argv) > 1 else 16
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 8
     run_mib = int(sys.argv[3]) if len(sys.argv) > 3 else 64
+    alloc = sys.argv[4] if len(sys.argv) > 4 else "torch"
     G = 1 << 30
     dev = torch.device("cuda:0")
-    host = torch.empty(slab_gib * G, dtype=torch.uint8, pin_memory=True)
+    if alloc == "lib":                                     # the library's CPU block buffer allocation
+        import ctypes
+        torch.cuda.init()
+        rt = ctypes.CDLL("libcudart.so.12")
+        ptr = ctypes.c_void_p()
+        assert rt.cudaHostAlloc(ctypes.byref(ptr), ctypes.c_size_t(slab_gib * G), 1 | 2) == 0   # Portable|Mapped
+        buf = (ctypes.c_uint8 * (slab_gib * G)).from_address(ptr.value)
+        host = torch.frombuffer(buf, dtype=torch.uint8)
+        assert host.is_pinned()
+    else:
+        host = torch.empty(slab_gib * G, dtype=torch.uint8, pin_memory=True)
     host.fill_(1)                                          # first touch: every page backed before timing
     d_up = torch.empty(G, dtype=torch.uint8, device=dev)
     d_off = torch.empty(G, dtype=torch.uint8, device=dev)
@@ -65,7 +78,7 @@ def main():
     for name, f in modes.items():
         pair(*f(0))                                        # warm-up
         res = [pair(*f(k)) for k in range(reps)]
-        out = {"mode": name, "slab_gib": slab_gib, "run_mib": run_mib if name == "runs" else None, "reps": reps}
+        out = {"mode": name, "alloc": alloc, "slab_gib": slab_gib, "run_mib": run_mib if name == "runs" else None, "reps": reps}
         for i, key in enumerate(("h2d_gbs", "d2h_gbs", "pair_gbs")):
             xs = [r[i] for r in res]
             out[key] = {"best": round(max(xs), 2), "median": round(statistics.median(xs), 2)}
