@@ -709,6 +709,15 @@ def run_ours(args):
             if k in kern:
                 link_roof[k + "_frac_of_unidir_peak"] = kern[k]["achieved_gbs"] / link[pk]
                 link_roof[k + "_frac_of_bidir_share"] = kern[k]["achieved_gbs"] / bi
+    if self_peer and kern_only:
+        # same-GPU peer slab: the offload and upload kernels read and write the same HBM at once, so each kernel's own
+        # duration shows it sharing the bandwidth; the step's bound is HBM for both directions together
+        hbm_bytes = 2 * all_bytes / world                    # every moved byte is read once and written once
+        roof_step = {"bound": "hbm", "achieved": hbm_bytes / (dev_total_ms * 1e-3) / 1e9, "peak": hbm,
+                     "peak_source": hbm_src, "how": "both directions' HBM read + write bytes / the timed region's "
+                     "device time (the two peer kernels overlap and share HBM)"}
+        roof_step["frac"] = roof_step["achieved"] / hbm if hbm else None
+        roof["step_hbm"] = roof_step
     cpu = None
     if not args.no_cpu_baseline:               # rank 0, after the timed region (the other ranks wait at the barrier)
         cpu = cpu_baseline(cfg, args.cpu_seconds, G)
