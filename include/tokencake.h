@@ -60,10 +60,12 @@ typedef enum {
 
 typedef enum {
     TC_XFER_AUTO = 0,    /* per direction: STAGED, the path measured fastest for the cycle on B200 (re-measured on
-                            this box by tc_calibrate), except that a batch of <= 2 MiB takes DIRECT (one launch,
-                            lower latency) */
+                            this box by tc_calibrate), except that a batch up to the small-batch crossover (2 MiB
+                            until tc_calibrate measures it per direction) takes DIRECT (one launch, lower latency;
+                            DESIGN.md §6) */
     TC_XFER_DIRECT = 1,  /* one SM kernel reads/writes mapped pinned host memory over the host link */
-    TC_XFER_STAGED = 2,  /* TMA gather/scatter to a device staging buffer + batched copy-engine DMA */
+    TC_XFER_STAGED = 2,  /* TMA gather/scatter to a device staging buffer + one copy-engine DMA per contiguous run
+                            of host slots */
     TC_XFER_COPY = 3     /* the copy engine moves each block as one strided DMA (2L rows of C bytes, row pitch N*C in
                             the pool) straight between the pool and its pinned slot; a small kernel rewrites the
                             block table (offload: before the DMA; upload: after it) */
@@ -182,7 +184,8 @@ tc_status tc_agent_free(tc_pool *p, int32_t agent);
 /* ---- the hot path (a2-a8) ----------------------------------------------------------------------------------- */
 /* a2+a3: offload block_ids[0..n) (on-GPU blocks exclusively owned by the agent) to pinned host slots from the
    CPU block buffer; gather all 2L chunks of each block in one kernel launch; table entries -> -1 (device table
-   written by the kernel epilogue); source blocks PENDING until tc_sync.  *out = new handle. */
+   written by the kernel epilogue); source blocks PENDING until a retirement point that covers this call — tc_sync,
+   tc_retire, tc_retire_lag (A8, A8', A8'').  *out = new handle. */
 tc_status tc_offload(tc_pool *p, int32_t agent, const int32_t *block_ids, int64_t n, tc_handle *out);
 /* a5+a6: allocate n new blocks (rule of tc_alloc) and scatter the handle's host copy into them; the kernel's fused
    epilogue writes table[agent][pos_i] = out_new_ids[i] (new_ids[i] replaces block_ids[i], A6).  Upload waits
