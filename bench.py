@@ -605,6 +605,9 @@ def run_ours(args):
         with open(os.environ["TC_DUMP_TIMELINE"], "w") as f:
             json.dump(tl_raw, f)
 
+    # the link re-measured after the timed region (all ranks at once, best of 3): a box whose link drifts shows it
+    # here, next to the pre-loop best-of-10 peak that is the denominator of roofline_link
+    link_after = None if (args.quick or not link) else hostlink_peak(torch, dev, reps=3)
     sweep = None
     if cfg.name == "c5" and not args.no_sweep:      # BASELINE configs[4]: 1-512 blocks per offload (every rank)
         if dist is not None:
@@ -768,6 +771,7 @@ def run_ours(args):
         "per_cycle_drain": other,
         "hostlink_peak": link,
         "hostlink_peak_alone": link_alone,
+        "hostlink_peak_after": link_after,
         "sweep": sweep,
         "roofline": roof,
         "roofline_link": link_roof,
