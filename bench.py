@@ -76,6 +76,9 @@ def parse():
                     help="c4 on one GPU: run one rank's shard of a G-GPU head-sharded run (G = 1, 2, 4, 8) — the work "
                          "each GPU of that run does, alone on this GPU and its own host link (per-GPU flatness)")
     ap.add_argument("--shard-rank", type=int, default=0, help="with --head-shards: which rank's shard (0 .. G-1)")
+    ap.add_argument("--host-frac", type=float, default=0.0,
+                    help="pinned host slots as a fraction of N (default: the config's, 0.25 for C3-C5) — a study "
+                         "knob: the paper's box had 100 GB of host swap per GPU (P:674)")
     ap.add_argument("--dry-run", action="store_true",
                     help="launcher / rendezvous / workload-plan check without a GPU: every rank joins the process group "
                          "(gloo), rank 0 prints the plan line (n_gpus, head shards, per-rank rows, cpu_baseline)")
@@ -389,6 +392,8 @@ def run_ours(args):
                           "staged": (tcb.XFER_STAGED,) * 2, "copy": (tcb.XFER_COPY,) * 2,
                           "mixed": (tcb.XFER_DIRECT, tcb.XFER_STAGED),
                           "mixed_rev": (tcb.XFER_STAGED, tcb.XFER_DIRECT)}[args.mode]
+    if args.host_frac > 0:
+        cfg = cfg.scaled(cfg.N, host_slots=max(1, int(cfg.N * args.host_frac)))
     S = cfg.host_slots()
     if args.gpus != world and rank == 0:
         print(f"bench.py: --gpus {args.gpus} but {world} rank(s) in this launch; n_gpus reports {world}",
@@ -426,6 +431,7 @@ def run_ours(args):
 
     drains = [0]                               # refused cycles retried after a tc_sync
     ladders = [0]                              # refused cycles retried after a tc_retire (then maybe the sync)
+    refused = {"nohost": 0, "noblocks": 0}     # why (first refusal of each laddered cycle)
     lag = [1]
 
     def cycle(record=None, retire="sync"):
@@ -455,6 +461,7 @@ def run_ours(args):
                         raise                       # retire the previous cycle's transfers and retry, then drain
                     pool.retire(1)
                     ladders[0] += 1
+                    refused["nohost" if e.status == tcb.E_NOHOST else "noblocks"] += 1
                     try:
                         _, out_h = pool.cycle_arrays(hs, uoff, ags, ooff, ids)
                     except tcb.TcError as e2:
@@ -521,6 +528,7 @@ def run_ours(args):
         for e, st in zip(e0, (ups, offs_)):
             e.record(st)
         drains[0] = ladders[0] = 0
+        refused["nohost"] = refused["noblocks"] = 0
         for k in range(args.steps):
             th = time.perf_counter()
             nu, no = cycle(retire="retire")
@@ -737,6 +745,7 @@ def run_ours(args):
                           "not touch" if args.retire == "each" else
                           "flushed between steps (256 MiB write, outside the step events)"),
                    "retire_lag": lag[0] if args.retire == "each" else None,
+                   "ladder_refusals": dict(refused) if args.retire == "each" else None,
                    "step": (f"tc_cycle + tc_retire_lag({lag[0]}) (retire the transfers enqueued before the "
                             f"{lag[0]}-th previous point, do not drain the last {lag[0]} cycles'); "
                             "a cycle the host buffer / free blocks refuse is retried after a tc_retire, then once "

@@ -224,6 +224,7 @@ tc_status Pool::create(const tc_pool_desc &d) {
     device = d.device;
     meta_only = d.device < 0;
     check = env_int("TC_CHECK", 0) != 0;
+    fine_off = env_int("TC_FINE_DEPS", 1) == 0;
     unbuffered = d.unbuffered != 0;
     next_slot = S;
     mode_d2h = d.xfer_d2h;
@@ -573,11 +574,44 @@ tc_status Pool::xfer_init(XferJob &j, bool gather, int32_t mode, const std::vect
         j.sk = j.s;
         return TC_OK;
     }
-    int32_t e0;
-    tc_status st = ev_rec(s, &e0);                  // the aux stream starts after the main stream's waits
-    if (st != TC_OK) return st;
-    TC_CUDA(cudaStreamWaitEvent(j.sk, events[e0], 0), "aux wait");
+    j.need_hop = true;                               // phase A: the aux stream starts after the main stream's waits
     return TC_OK;
+}
+
+// Fine-grained dependencies: the items (one agent's offload, one handle's upload) held by blocks [a, b) of the job.
+tc_status Pool::piece_waits(const XferJob &j, int64_t a, int64_t b, cudaStream_t st) {
+    if (!j.item_dep) return TC_OK;
+    int64_t k = std::upper_bound(j.item_off, j.item_off + j.n_items + 1, a) - j.item_off - 1;
+    int32_t last = -1;
+    for (; k < j.n_items && j.item_off[k] < b; ++k) {
+        const int32_t e = j.item_dep[k];
+        if (e >= 0 && e != last) TC_CUDA(cudaStreamWaitEvent(st, events[e], 0), "item wait");
+        if (e >= 0) last = e;
+    }
+    return TC_OK;
+}
+
+// A staged job of several pieces waits per piece for the items it holds and marks each piece's end, so a batch's
+// first items do not wait for its last items' dependencies, and a handle completes with the piece holding its last
+// block instead of with the whole batch (a cycle's uploads can start on the first offloads of the previous cycle
+// as soon as their pieces are on the host).  Ordering only: ids and bytes are unchanged.
+bool Pool::fine_grained(XferJob &j, const int64_t *item_off, int32_t n_items, const std::vector<int32_t> &deps) {
+    if (j.mode != TC_XFER_STAGED || j.npieces < 2 || fine_off) return false;
+    j.item_off = item_off;
+    j.item_dep = deps.data();
+    j.n_items = n_items;
+    j.piece_done.assign(j.npieces, -1);
+    return true;
+}
+
+// Per-item completion events of a fine-grained job: the piece holding the item's last block.
+void Pool::item_events(const XferJob &j, std::vector<int32_t> &out) const {
+    out.resize(j.n_items);
+    for (int32_t k = 0; k < j.n_items; ++k) {
+        const int64_t last = j.item_off[k + 1] - 1;
+        const int64_t p = std::upper_bound(j.cut.begin(), j.cut.end(), last) - j.cut.begin() - 1;
+        out[k] = j.piece_done[p];
+    }
 }
 
 // AUTO: the path measured fastest for a full scheduling cycle on B200 (both directions concurrently).
@@ -835,12 +869,18 @@ tc_status Pool::xfer_phase_a(XferJob &j) {
         if ((st = launch_descs(j.gather, kind, path, d, j.n, j.s)) != TC_OK) return st;
         return span_end(j.s, kind, t0, j.n * B);
     }
+    if (j.need_hop) {                                // the aux stream starts after the main stream's waits
+        int32_t e0;
+        if ((st = ev_rec(j.s, &e0)) != TC_OK) return st;
+        TC_CUDA(cudaStreamWaitEvent(j.sk, events[e0], 0), "aux wait");
+    }
     std::vector<int32_t> done(j.ring_reuse ? j.npieces : 0, -1);
     for (int64_t p = 0; p < j.npieces; ++p) {
         const int64_t a = j.cut[p], b = j.cut[p + 1];
         char *base = xfer_base(j, p);
         if (j.gather) {
             if (j.ring_reuse && p >= 2) TC_CUDA(cudaStreamWaitEvent(j.sk, events[done[p - 2]], 0), "ring reuse");
+            if ((st = piece_waits(j, a, b, j.sk)) != TC_OK) return st;       // the gather reads the items' blocks
             if ((st = xfer_kernel(j, a, b, base)) != TC_OK) return st;
             // the D2H copy of a piece is issued right after its gather, so the link starts after the small
             // head piece's gather and a handful of API calls
@@ -850,14 +890,20 @@ tc_status Pool::xfer_phase_a(XferJob &j) {
             }
             if ((st = xfer_copy(j, a, b, base)) != TC_OK) return st;
             if (j.ring_reuse && (st = ev_rec(j.s, &done[p])) != TC_OK) return st;
+            if (j.item_dep) {                            // piece p is on the host
+                if (j.ring_reuse) j.piece_done[p] = done[p];
+                else if ((st = ev_rec(j.s, &j.piece_done[p])) != TC_OK) return st;
+            }
         } else {
             if (j.ring_reuse && p >= 2) TC_CUDA(cudaStreamWaitEvent(j.s, events[done[p - 2]], 0), "ring reuse");
+            if ((st = piece_waits(j, a, b, j.s)) != TC_OK) return st;        // the H2D reads the items' host slots
             if ((st = xfer_copy(j, a, b, base)) != TC_OK) return st;
             if (j.sk != j.s && (st = ev_rec(j.s, &j.ev[p])) != TC_OK) return st;
             if (j.ring_reuse) {
                 TC_CUDA(cudaStreamWaitEvent(j.sk, events[j.ev[p]], 0), "H2D->scatter wait");
                 if ((st = xfer_kernel(j, a, b, base)) != TC_OK) return st;
                 if ((st = ev_rec(j.sk, &done[p])) != TC_OK) return st;
+                if (j.item_dep) j.piece_done[p] = done[p];   // piece p is in the pool, its table entries remapped
             }
         }
     }
@@ -873,6 +919,7 @@ tc_status Pool::xfer_phase_b(XferJob &j) {
             const int64_t a = j.cut[p], b = j.cut[p + 1];
             if (j.sk != j.s) TC_CUDA(cudaStreamWaitEvent(j.sk, events[j.ev[p]], 0), "H2D->scatter wait");
             if ((st = xfer_kernel(j, a, b, xfer_base(j, p))) != TC_OK) return st;
+            if (j.item_dep && (st = ev_rec(j.sk, &j.piece_done[p])) != TC_OK) return st;
         }
         if (j.half < 0 && j.sk != j.s) {              // the upload completes when its last scatter has
             int32_t last;
@@ -1115,7 +1162,7 @@ tc_status Pool::join(cudaStream_t s, int32_t ev) {
 
 // GPU-side dependencies of an offload: the compute stream (the agents' last decode writes) and any upload into
 // these agents since the last sync.
-tc_status Pool::offload_waits(const OffPlan &P) {
+tc_status Pool::offload_waits(const OffPlan &P, bool ups) {
     if (s_compute) {
         TC_CUDA(cudaEventRecord(ev_compute, s_compute), "compute event");
         TC_CUDA(cudaStreamWaitEvent(s_off, ev_compute, 0), "compute wait");
@@ -1124,7 +1171,7 @@ tc_status Pool::offload_waits(const OffPlan &P) {
     for (int32_t k = 0; k < P.na; ++k) {
         if (cudaEvent_t pe = agents[P.ags[k]].push_ev)
             TC_CUDA(cudaStreamWaitEvent(s_off_k, pe, 0), "table push->offload wait");
-        const int32_t ue = agents[P.ags[k]].up_event;
+        const int32_t ue = ups ? agents[P.ags[k]].up_event : -1;
         if (ue >= 0) {
             TC_CUDA(cudaStreamWaitEvent(s_off, events[ue], 0), "upload->offload wait");
             TC_CUDA(cudaStreamWaitEvent(s_off_k, events[ue], 0), "upload->offload wait");   // halves gathers
@@ -1135,7 +1182,7 @@ tc_status Pool::offload_waits(const OffPlan &P) {
 
 // commit (a3 logical effects + a4 pending free); ev = the offload's completion event
 // (no allocation: plan_offload built the handle records and grew every container this touches)
-void Pool::commit_offload(OffPlan &P, int32_t ev, tc_handle *out) {
+void Pool::commit_offload(OffPlan &P, int32_t ev, tc_handle *out, const std::vector<int32_t> *item_ev) {
     const int64_t n = P.off[P.na];
     if (!unbuffered) {
         slots.take(P.host_slots.data(), P.host_taken);
@@ -1155,7 +1202,7 @@ void Pool::commit_offload(OffPlan &P, int32_t ev, tc_handle *out) {
         pending_epoch.push_back(epoch_id);
         ++ag.live_offloads;
         const tc_handle h = next_handle++;
-        P.newh.at(h).ev = ev;
+        P.newh.at(h).ev = item_ev ? (*item_ev)[k] : ev;
         out[k] = h;
     }
     handles.merge(P.newh);                                 // splices the prebuilt nodes (no rehash: reserved)
@@ -1228,7 +1275,7 @@ tc_status Pool::upload_waits(const UpPlan &P) {          // A13: the upload wait
 }
 
 // commit (a5 allocation, a6 remap, a7 released slots); ev = the upload's completion event
-void Pool::commit_upload(UpPlan &P, int32_t ev, int32_t *out_ids) {
+void Pool::commit_upload(UpPlan &P, int32_t ev, int32_t *out_ids, const std::vector<int32_t> *item_ev) {
     if (P.n_fresh > 0) alloc.take_lowest(P.n_fresh, P.taken.data());   // == the planned ids (nothing changed since)
     for (int32_t k = 0; k < P.nh; ++k) {
         HandleRec &h = *P.hr[k];
@@ -1251,9 +1298,9 @@ void Pool::commit_upload(UpPlan &P, int32_t ev, int32_t *out_ids) {
         resv_active.erase(P.hs[k]);
         h.state = kUploaded;
         h.up_epoch = epoch_id;
-        h.ev = ev;
+        h.ev = item_ev ? (*item_ev)[k] : ev;
         --ag.live_offloads;
-        ag.up_event = ev;
+        ag.up_event = h.ev;
     }
     if (!meta_only) bytes_h2d += P.off[P.nh] * B;
 }
@@ -1267,19 +1314,31 @@ tc_status Pool::offload_batch(int32_t na, const int32_t *ags, const int64_t *off
     tc_status st = plan_offload(P, na, ags, off, ids);
     if (st != TC_OK) return st;
     int32_t ev = -1;
+    std::vector<int32_t> deps, item_ev;
+    bool fine = false;
     if (!meta_only) try {
-        if ((st = offload_waits(P)) != TC_OK) return st;
+        XferJob j;
+        const bool pt = peer.count > 0;
+        if ((st = xfer_init(j, true, mode_d2h, pt ? &P.ts.hdesc : &P.desc, pt ? &P.ts.hslot : &P.slot_of, s_off)) !=
+            TC_OK)
+            return st;
+        if (!pt) {
+            deps.resize(na);
+            for (int32_t k = 0; k < na; ++k) deps[k] = agents[ags[k]].up_event;
+            fine = fine_grained(j, off, na, deps);
+        }
+        if ((st = offload_waits(P, !fine)) != TC_OK) return st;
         int32_t pj;
         if ((st = peer_launch(true, P.ts.pdesc, s_off, &pj)) != TC_OK) return st;
-        if ((st = enqueue_xfer(true, mode_d2h, peer.count ? P.ts.hdesc : P.desc, peer.count ? P.ts.hslot : P.slot_of,
-                               s_off)) != TC_OK)
-            return st;
+        if ((st = xfer_phase_a(j)) != TC_OK) return st;
+        if ((st = xfer_phase_b(j)) != TC_OK) return st;
         if ((st = join(s_off, pj)) != TC_OK) return st;
         if ((st = ev_rec(s_off, &ev)) != TC_OK) return st;
+        if (fine) item_events(j, item_ev);
     } catch (const std::bad_alloc &) {
         return enqueue_oom();
     }
-    commit_offload(P, ev, out);
+    commit_offload(P, ev, out, fine ? &item_ev : nullptr);
     trace_calls(1, ags, out, off, na, s_off);
     return TC_OK;
 }
@@ -1292,19 +1351,31 @@ tc_status Pool::upload_batch(int32_t nh, const tc_handle *hs, const int64_t *off
     tc_status st = plan_upload(P, nh, hs, off);
     if (st != TC_OK) return st;
     int32_t ev = -1;
+    std::vector<int32_t> deps, item_ev;
+    bool fine = false;
     if (!meta_only) try {
-        if ((st = upload_waits(P)) != TC_OK) return st;
+        XferJob j;
+        const bool pt = peer.count > 0;
+        if ((st = xfer_init(j, false, mode_h2d, pt ? &P.ts.hdesc : &P.desc, pt ? &P.ts.hslot : &P.slot_of, s_up)) !=
+            TC_OK)
+            return st;
+        if (!pt) {
+            deps.resize(nh);
+            for (int32_t k = 0; k < nh; ++k) deps[k] = P.hr[k]->ev;
+            fine = fine_grained(j, off, nh, deps);
+        }
+        if (!fine && (st = upload_waits(P)) != TC_OK) return st;
         int32_t pj;
         if ((st = peer_launch(false, P.ts.pdesc, s_up, &pj)) != TC_OK) return st;
-        if ((st = enqueue_xfer(false, mode_h2d, peer.count ? P.ts.hdesc : P.desc, peer.count ? P.ts.hslot : P.slot_of,
-                               s_up)) != TC_OK)
-            return st;
+        if ((st = xfer_phase_a(j)) != TC_OK) return st;
+        if ((st = xfer_phase_b(j)) != TC_OK) return st;
         if ((st = join(s_up, pj)) != TC_OK) return st;
         if ((st = ev_rec(s_up, &ev)) != TC_OK) return st;
+        if (fine) item_events(j, item_ev);
     } catch (const std::bad_alloc &) {
         return enqueue_oom();
     }
-    commit_upload(P, ev, out_ids);
+    commit_upload(P, ev, out_ids, fine ? &item_ev : nullptr);
     trace_calls(2, nullptr, hs, off, nh, s_up);
     return TC_OK;
 }
@@ -1329,39 +1400,53 @@ tc_status Pool::cycle(int32_t nh, const tc_handle *hs, const int64_t *up_off, in
     if (na > 0 && (st = plan_offload(O, na, ags, off_off, ids)) != TC_OK) return st;
     trace("plans");
     int32_t ev_up = -1, ev_off = -1;
+    std::vector<int32_t> deps_u, deps_o, iev_u, iev_o;
+    bool fine_u = false, fine_o = false;
     if (!meta_only) try {
         XferJob ju, jo;
         int32_t pu = -1, po = -1;                                     // peer-tier parts (NEXT-2)
         const bool pt = peer.count > 0;
         if (nh > 0) {
-            if ((st = upload_waits(U)) != TC_OK) return st;
-            if ((st = peer_launch(false, U.ts.pdesc, s_up, &pu)) != TC_OK) return st;
             if ((st = xfer_init(ju, false, mode_h2d, pt ? &U.ts.hdesc : &U.desc, pt ? &U.ts.hslot : &U.slot_of,
                                 s_up)) != TC_OK)
                 return st;
+            if (!pt) {
+                deps_u.resize(nh);
+                for (int32_t k = 0; k < nh; ++k) deps_u[k] = U.hr[k]->ev;
+                fine_u = fine_grained(ju, up_off, nh, deps_u);
+            }
+            if (!fine_u && (st = upload_waits(U)) != TC_OK) return st;
+            if ((st = peer_launch(false, U.ts.pdesc, s_up, &pu)) != TC_OK) return st;
             if ((st = xfer_phase_a(ju)) != TC_OK) return st;          // H2D copies start first
         }
         if (na > 0) {
-            if ((st = offload_waits(O)) != TC_OK) return st;
-            if ((st = peer_launch(true, O.ts.pdesc, s_off, &po)) != TC_OK) return st;
             if ((st = xfer_init(jo, true, mode_d2h, pt ? &O.ts.hdesc : &O.desc, pt ? &O.ts.hslot : &O.slot_of,
                                 s_off)) != TC_OK)
                 return st;
+            if (!pt) {
+                deps_o.resize(na);
+                for (int32_t k = 0; k < na; ++k) deps_o[k] = agents[ags[k]].up_event;
+                fine_o = fine_grained(jo, off_off, na, deps_o);
+            }
+            if ((st = offload_waits(O, !fine_o)) != TC_OK) return st;
+            if ((st = peer_launch(true, O.ts.pdesc, s_off, &po)) != TC_OK) return st;
             if ((st = xfer_phase_a(jo)) != TC_OK) return st;          // gathers
             if ((st = xfer_phase_b(jo)) != TC_OK) return st;          // D2H copies
             if ((st = join(s_off, po)) != TC_OK) return st;
             if ((st = ev_rec(s_off, &ev_off)) != TC_OK) return st;
+            if (fine_o) item_events(jo, iev_o);
         }
         if (nh > 0) {
             if ((st = xfer_phase_b(ju)) != TC_OK) return st;          // scatters + remap
             if ((st = join(s_up, pu)) != TC_OK) return st;
             if ((st = ev_rec(s_up, &ev_up)) != TC_OK) return st;
+            if (fine_u) item_events(ju, iev_u);
         }
     } catch (const std::bad_alloc &) {
         return enqueue_oom();
     }
-    if (nh > 0) commit_upload(U, ev_up, out_ids);
-    if (na > 0) commit_offload(O, ev_off, out_h);
+    if (nh > 0) commit_upload(U, ev_up, out_ids, fine_u ? &iev_u : nullptr);
+    if (na > 0) commit_offload(O, ev_off, out_h, fine_o ? &iev_o : nullptr);
     if (nh > 0) trace_calls(2, nullptr, hs, up_off, nh, s_up);
     if (na > 0) trace_calls(1, ags, out_h, off_off, na, s_off);
     if (g_trace) {

@@ -258,11 +258,13 @@ struct Pool {
     tc_status peer_launch(bool gather, const std::vector<XferDesc> &pd, cudaStream_t s, int32_t *join_ev);
     tc_status join(cudaStream_t s, int32_t ev);
     tc_status plan_offload(OffPlan &P, int32_t na, const int32_t *ags, const int64_t *off, const int32_t *ids);
-    tc_status offload_waits(const OffPlan &P);
-    void commit_offload(OffPlan &P, int32_t ev, tc_handle *out);
+    // GPU-side dependencies of an offload; ups = also the agents' last uploads (false: the job waits per piece)
+    tc_status offload_waits(const OffPlan &P, bool ups = true);
+    // ev = the batch's completion event; item_ev (optional) = per-item completion events (fine-grained jobs)
+    void commit_offload(OffPlan &P, int32_t ev, tc_handle *out, const std::vector<int32_t> *item_ev = nullptr);
     tc_status plan_upload(UpPlan &P, int32_t nh, const tc_handle *hs, const int64_t *off);
     tc_status upload_waits(const UpPlan &P);
-    void commit_upload(UpPlan &P, int32_t ev, int32_t *out_ids);
+    void commit_upload(UpPlan &P, int32_t ev, int32_t *out_ids, const std::vector<int32_t> *item_ev = nullptr);
     tc_status query(tc_handle h, bool wait);
     tc_status stream_wait(tc_handle h, cudaStream_t s);
     tc_status sync();
@@ -293,7 +295,20 @@ struct Pool {
         std::vector<int64_t> cut;            // piece p = blocks [cut[p], cut[p+1])
         char *stg = nullptr;
         std::vector<int32_t> ev;
+        bool need_hop = false;               // the aux stream starts after the main stream's waits (phase A)
+        // Fine-grained dependencies (a staged batch of several pieces): item k (one agent's offload / one handle's
+        // upload) = blocks [item_off[k], item_off[k+1]); a piece waits only for item_dep[] of the items it holds,
+        // and piece_done[p] marks the end of piece p's whole transfer (the items' completion events).
+        const int64_t *item_off = nullptr;
+        const int32_t *item_dep = nullptr;
+        int32_t n_items = 0;
+        std::vector<int32_t> piece_done;
     };
+    bool fine_off = false;                   // TC_FINE_DEPS=0: batch-granular dependencies (A/B)
+    tc_status piece_waits(const XferJob &j, int64_t a, int64_t b, cudaStream_t st);
+    // fine-grained mode for a job after xfer_init (staged, several pieces, no peer-tier part); deps per item
+    bool fine_grained(XferJob &j, const int64_t *item_off, int32_t n_items, const std::vector<int32_t> &deps);
+    void item_events(const XferJob &j, std::vector<int32_t> &out) const;
     char *xfer_base(const XferJob &j, int64_t p) const;
     // host address (and its device mapping) of a host slot id: the CPU block buffer, or an ablation slab
     char *host_ptr(int64_t slot) const;

@@ -20,6 +20,7 @@ pytestmark = pytest.mark.gpu
 
 import paper_2510_18586_b200 as tcb  # noqa: E402
 from oracle import BytesStore, OraclePool  # noqa: E402
+from oracle.pool import OFFLOADED  # noqa: E402
 from workloads import content  # noqa: E402
 from workloads.replay import Replayer  # noqa: E402
 from workloads.scripts import fuzz_script  # noqa: E402
@@ -173,4 +174,99 @@ def test_device_tier_on_destroyed_caller_stream_does_not_poison_sync():
     pool0 = content.pool_bytes(1, L, N, 16, H, D)
     assert np.array_equal(dst.cpu().numpy().reshape(5, L, 2, c.chunk_bytes),
                           np.take(pool0, ids, axis=2).transpose(2, 0, 1, 3))
+    c.close()
+
+
+def _piece_pool(kind, monkeypatch, L, H, D, N, S, seed):
+    """A staged pool whose multi-block batches run as several pieces: `ring` = a 4-block staging buffer (2-block
+    halves reused in turn), `pieces` = a large buffer cut into one-block pieces (TC_PIECE_KIB), no staging halves."""
+    T = 16
+    B = 2 * L * T * H * D * 2
+    if kind == "pieces":
+        monkeypatch.setenv("TC_PIECE_KIB", str(max(1, B // 1024)))
+        monkeypatch.setenv("TC_STAGING_HALVES", "0")
+        staging = 64 * B
+    else:
+        staging = 4 * B
+    c = tcb.Pool(L, H, D, T, "bf16", N, device=0, host_slots=S, n_classes=2, xfer_d2h=tcb.XFER_STAGED,
+                 xfer_h2d=tcb.XFER_STAGED, staging_bytes=staging)
+    c.fill(seed)
+    return c
+
+
+@pytest.mark.parametrize("kind", ["ring", "pieces"])
+def test_multi_piece_upload_waits_for_each_items_offload(kind, monkeypatch):
+    """A batch upload of several pieces issued right behind the batch offload it undoes, with the offload's copies
+    held back by a long sleep on the offload stream: each upload piece waits for the offload pieces holding its
+    handles' blocks (per-piece dependencies), so every scattered block equals the oracle's bytes.  A piece that did
+    not wait would copy host slots the D2H had not written yet."""
+    L, H, D, N, S = 2, 2, 64, 96, 40
+    pool0 = content.pool_bytes(5, L, N, 16, H, D)
+    o = OraclePool(N, S, n_classes=2, store=BytesStore(pool0, S))
+    c = _piece_pool(kind, monkeypatch, L, H, D, N, S, 5)
+    for x in (o, c):
+        for a in range(8):
+            x.agent_add(a, 0)
+    for rnd in range(3):                              # interleaved growth: scattered ids
+        for a in range(8):
+            assert o.alloc(a, 1) == list(c.alloc(a, 1))
+    for rep in range(3):
+        # decoys 4-7 first pass through the same host slots (and allocate the staging buffers, whose cudaMalloc
+        # would synchronise the device): an upload that did not wait would read their bytes
+        items = [(a, o.block_table(a)) for a in range(4, 8)]
+        assert c.offload_batch(items) == o.offload_batch(items)
+        hs = [h for h in sorted(o.handles) if o.handles[h].state == OFFLOADED]
+        assert o.upload_batch(hs) == c.upload_batch(hs)
+        c.sync()
+        o.sync()
+        _, off_s = c.streams()
+        with torch.cuda.stream(torch.cuda.ExternalStream(off_s, device=0)):
+            torch.cuda._sleep(SLEEP_CYCLES)           # the offload's copies queue behind this
+        items = [(a, o.block_table(a)) for a in range(4)]
+        assert c.offload_batch(items) == o.offload_batch(items)
+        hs = [h for h in sorted(o.handles) if o.handles[h].state == OFFLOADED]
+        new_o, new_c = o.upload_batch(hs), c.upload_batch(hs)   # no host wait in between
+        assert new_o == new_c, rep
+        c.sync()
+        o.sync()
+        assert np.array_equal(c.kv_tensor().cpu().numpy(), o.store.pool), (kind, rep)
+        for a in range(8):
+            assert c.block_table(a) == o.block_table(a)
+    c.close()
+
+
+@pytest.mark.parametrize("kind", ["ring", "pieces"])
+def test_multi_piece_offload_waits_for_each_items_upload(kind, monkeypatch):
+    """A batch offload of several pieces issued right behind the batch upload that brought its agents back, with the
+    upload's copies held back by a long sleep on the upload stream: each gather piece waits for the upload pieces
+    holding its agents' blocks, so every offloaded host image equals the oracle's.  A piece that did not wait would
+    gather blocks the scatter had not written yet."""
+    L, H, D, N, S = 2, 2, 64, 96, 40
+    pool0 = content.pool_bytes(6, L, N, 16, H, D)
+    o = OraclePool(N, S, n_classes=2, store=BytesStore(pool0, S))
+    c = _piece_pool(kind, monkeypatch, L, H, D, N, S, 6)
+    for x in (o, c):
+        for a in range(4):
+            x.agent_add(a, 0)
+    for rnd in range(3):
+        for a in range(4):
+            assert o.alloc(a, 1) == list(c.alloc(a, 1))
+    items = [(a, o.block_table(a)) for a in range(4)]
+    assert c.offload_batch(items) == o.offload_batch(items)
+    for rep in range(3):
+        c.sync()
+        o.sync()
+        up_s, _ = c.streams()
+        with torch.cuda.stream(torch.cuda.ExternalStream(up_s, device=0)):
+            torch.cuda._sleep(SLEEP_CYCLES)           # the upload's copies queue behind this
+        hs = [h for h in sorted(o.handles) if o.handles[h].state == OFFLOADED]
+        assert o.upload_batch(hs) == c.upload_batch(hs)
+        items = [(a, o.block_table(a)) for a in range(4)]
+        got = c.offload_batch(items)                  # no host wait in between
+        assert got == o.offload_batch(items)
+        for h in got:
+            c.wait(h)
+            for i, s in enumerate(o.handles[h].slots):
+                assert np.array_equal(c.handle_host_bytes(h, i), o.store.host[s]), (kind, rep, h, i)
+    c.sync()
     c.close()
