@@ -225,6 +225,7 @@ tc_status Pool::create(const tc_pool_desc &d) {
     meta_only = d.device < 0;
     check = env_int("TC_CHECK", 0) != 0;
     fine_off = env_int("TC_FINE_DEPS", 1) == 0;
+    min_piece_bytes = env_int("TC_MIN_PIECE_MIB", 64) * (1ll << 20);
     unbuffered = d.unbuffered != 0;
     next_slot = S;
     mode_d2h = d.xfer_d2h;
@@ -521,7 +522,8 @@ char *Pool::ring_alloc(int64_t bytes, char **dev_ptr) {
 // batch larger than the staging buffer runs double-buffered pieces of half the buffer, issued interleaved in phase
 // A (B does nothing).
 tc_status Pool::xfer_init(XferJob &j, bool gather, int32_t mode, const std::vector<XferDesc> *desc,
-                          const std::vector<int64_t> *slot_of, cudaStream_t s) {
+                          const std::vector<int64_t> *slot_of, cudaStream_t s, const int64_t *item_off,
+                          int32_t n_items) {
     j.gather = gather;
     j.mode = (slot_of == nullptr || slot_of->empty()) ? TC_XFER_DIRECT : mode;
     j.desc = desc;
@@ -540,11 +542,28 @@ tc_status Pool::xfer_init(XferJob &j, bool gather, int32_t mode, const std::vect
     j.ring_reuse = j.n > cap;
     const int64_t edge = head_bytes > 0 ? std::max<int64_t>(1, head_bytes / B) : 0;   // head / tail blocks
     const int64_t big = std::max<int64_t>(1, piece_bytes / B);
+    // With the items' block offsets (a batch of several agents / handles, fine-grained dependencies on), a piece
+    // ends on the last item boundary inside its size limit when that leaves it at least min_piece_bytes: an item's
+    // last block then lands with its own piece instead of with the next item's first blocks, so its per-handle
+    // completion (below) comes sooner.  Ids and bytes do not depend on the cuts.
+    const bool align = item_off && n_items > 0 && !fine_off;
+    const int64_t min_blocks = std::max<int64_t>(1, min_piece_bytes / B);
+    auto cut_by = [&](int64_t step) {
+        for (int64_t a = 0; a < j.n;) {
+            j.cut.push_back(a);
+            int64_t e = std::min(j.n, a + step);
+            if (align && e < j.n) {
+                const int64_t *q = std::upper_bound(item_off, item_off + n_items + 1, e) - 1;   // last end <= e
+                if (*q > a && *q - a >= min_blocks) e = *q;
+            }
+            a = e;
+        }
+    };
     if (j.ring_reuse) {
-        const int64_t pb = std::max<int64_t>(1, cap / 2);
-        for (int64_t a = 0; a < j.n; a += pb) j.cut.push_back(a);
+        j.pb = std::max<int64_t>(1, cap / 2);
+        cut_by(j.pb);
     } else if (edge == 0) {
-        for (int64_t a = 0; a < j.n; a += big) j.cut.push_back(a);
+        cut_by(big);
     } else if (gather) {
         j.cut.push_back(0);
         for (int64_t a = std::min(edge, j.n); a < j.n; a += big) j.cut.push_back(a);
@@ -778,8 +797,7 @@ tc_status Pool::xfer_copy2d(XferJob &j) {
 // Staging address of piece p: contiguous by block index, or one of two halves when double-buffering.
 char *Pool::xfer_base(const XferJob &j, int64_t p) const {
     if (!j.ring_reuse) return j.stg + j.cut[p] * B;
-    const int64_t pb = j.cut[1] - j.cut[0];
-    return j.stg + (p % 2) * pb * B;
+    return j.stg + (p % 2) * j.pb * B;                 // pieces alternate the two halves (each <= pb blocks)
 }
 
 tc_status Pool::ev_rec(cudaStream_t st, int32_t *out) {
@@ -1319,8 +1337,8 @@ tc_status Pool::offload_batch(int32_t na, const int32_t *ags, const int64_t *off
     if (!meta_only) try {
         XferJob j;
         const bool pt = peer.count > 0;
-        if ((st = xfer_init(j, true, mode_d2h, pt ? &P.ts.hdesc : &P.desc, pt ? &P.ts.hslot : &P.slot_of, s_off)) !=
-            TC_OK)
+        if ((st = xfer_init(j, true, mode_d2h, pt ? &P.ts.hdesc : &P.desc, pt ? &P.ts.hslot : &P.slot_of, s_off,
+                            pt ? nullptr : off, na)) != TC_OK)
             return st;
         if (!pt) {
             deps.resize(na);
@@ -1356,8 +1374,8 @@ tc_status Pool::upload_batch(int32_t nh, const tc_handle *hs, const int64_t *off
     if (!meta_only) try {
         XferJob j;
         const bool pt = peer.count > 0;
-        if ((st = xfer_init(j, false, mode_h2d, pt ? &P.ts.hdesc : &P.desc, pt ? &P.ts.hslot : &P.slot_of, s_up)) !=
-            TC_OK)
+        if ((st = xfer_init(j, false, mode_h2d, pt ? &P.ts.hdesc : &P.desc, pt ? &P.ts.hslot : &P.slot_of, s_up,
+                            pt ? nullptr : off, nh)) != TC_OK)
             return st;
         if (!pt) {
             deps.resize(nh);
@@ -1408,7 +1426,7 @@ tc_status Pool::cycle(int32_t nh, const tc_handle *hs, const int64_t *up_off, in
         const bool pt = peer.count > 0;
         if (nh > 0) {
             if ((st = xfer_init(ju, false, mode_h2d, pt ? &U.ts.hdesc : &U.desc, pt ? &U.ts.hslot : &U.slot_of,
-                                s_up)) != TC_OK)
+                                s_up, pt ? nullptr : up_off, nh)) != TC_OK)
                 return st;
             if (!pt) {
                 deps_u.resize(nh);
@@ -1421,7 +1439,7 @@ tc_status Pool::cycle(int32_t nh, const tc_handle *hs, const int64_t *up_off, in
         }
         if (na > 0) {
             if ((st = xfer_init(jo, true, mode_d2h, pt ? &O.ts.hdesc : &O.desc, pt ? &O.ts.hslot : &O.slot_of,
-                                s_off)) != TC_OK)
+                                s_off, pt ? nullptr : off_off, na)) != TC_OK)
                 return st;
             if (!pt) {
                 deps_o.resize(na);

@@ -296,6 +296,7 @@ struct Pool {
         char *stg = nullptr;
         std::vector<int32_t> ev;
         bool need_hop = false;               // the aux stream starts after the main stream's waits (phase A)
+        int64_t pb = 0;                      // ring reuse: blocks per staging half (pieces are at most this)
         // Fine-grained dependencies (a staged batch of several pieces): item k (one agent's offload / one handle's
         // upload) = blocks [item_off[k], item_off[k+1]); a piece waits only for item_dep[] of the items it holds,
         // and piece_done[p] marks the end of piece p's whole transfer (the items' completion events).
@@ -321,8 +322,11 @@ struct Pool {
     bool unbuffered = false;
     std::map<int64_t, ExtraSlab> extra;      // first slot id -> slab
     int64_t next_slot = 0;
+    // item_off (optional, n_items + 1 block offsets): piece cuts fall on item boundaries where they can (below)
     tc_status xfer_init(XferJob &j, bool gather, int32_t mode, const std::vector<XferDesc> *desc,
-                        const std::vector<int64_t> *slot_of, cudaStream_t s);
+                        const std::vector<int64_t> *slot_of, cudaStream_t s, const int64_t *item_off = nullptr,
+                        int32_t n_items = 0);
+    int64_t min_piece_bytes = 64ll << 20;    // an item-aligned cut never leaves a piece smaller than this
     tc_status xfer_phase_a(XferJob &j);
     tc_status xfer_phase_b(XferJob &j);
     tc_status xfer_copy(XferJob &j, int64_t a, int64_t b, char *base);

@@ -179,9 +179,13 @@ def test_device_tier_on_destroyed_caller_stream_does_not_poison_sync():
 
 def _piece_pool(kind, monkeypatch, L, H, D, N, S, seed):
     """A staged pool whose multi-block batches run as several pieces: `ring` = a 4-block staging buffer (2-block
-    halves reused in turn), `pieces` = a large buffer cut into one-block pieces (TC_PIECE_KIB), no staging halves."""
+    halves reused in turn), `pieces` = a large buffer cut into one-block pieces (TC_PIECE_KIB), no staging halves;
+    `*_aligned`: pieces also end on item boundaries (TC_MIN_PIECE_MIB=0, i.e. no minimum piece size)."""
     T = 16
     B = 2 * L * T * H * D * 2
+    if kind.endswith("_aligned"):
+        monkeypatch.setenv("TC_MIN_PIECE_MIB", "0")
+        kind = kind[:-len("_aligned")]
     if kind == "pieces":
         monkeypatch.setenv("TC_PIECE_KIB", str(max(1, B // 1024)))
         monkeypatch.setenv("TC_STAGING_HALVES", "0")
@@ -194,7 +198,7 @@ def _piece_pool(kind, monkeypatch, L, H, D, N, S, seed):
     return c
 
 
-@pytest.mark.parametrize("kind", ["ring", "pieces"])
+@pytest.mark.parametrize("kind", ["ring", "pieces", "ring_aligned", "pieces_aligned"])
 def test_multi_piece_upload_waits_for_each_items_offload(kind, monkeypatch):
     """A batch upload of several pieces issued right behind the batch offload it undoes, with the offload's copies
     held back by a long sleep on the offload stream: each upload piece waits for the offload pieces holding its
@@ -207,9 +211,10 @@ def test_multi_piece_upload_waits_for_each_items_offload(kind, monkeypatch):
     for x in (o, c):
         for a in range(8):
             x.agent_add(a, 0)
-    for rnd in range(3):                              # interleaved growth: scattered ids
+    for rnd in range(4):                              # interleaved growth: scattered ids, 1-4 blocks per agent
         for a in range(8):
-            assert o.alloc(a, 1) == list(c.alloc(a, 1))
+            if rnd <= a % 4:
+                assert o.alloc(a, 1) == list(c.alloc(a, 1))
     for rep in range(3):
         # decoys 4-7 first pass through the same host slots (and allocate the staging buffers, whose cudaMalloc
         # would synchronise the device): an upload that did not wait would read their bytes
@@ -235,7 +240,7 @@ def test_multi_piece_upload_waits_for_each_items_offload(kind, monkeypatch):
     c.close()
 
 
-@pytest.mark.parametrize("kind", ["ring", "pieces"])
+@pytest.mark.parametrize("kind", ["ring", "pieces", "ring_aligned", "pieces_aligned"])
 def test_multi_piece_offload_waits_for_each_items_upload(kind, monkeypatch):
     """A batch offload of several pieces issued right behind the batch upload that brought its agents back, with the
     upload's copies held back by a long sleep on the upload stream: each gather piece waits for the upload pieces
@@ -248,9 +253,10 @@ def test_multi_piece_offload_waits_for_each_items_upload(kind, monkeypatch):
     for x in (o, c):
         for a in range(4):
             x.agent_add(a, 0)
-    for rnd in range(3):
+    for rnd in range(4):                              # 1-4 blocks per agent
         for a in range(4):
-            assert o.alloc(a, 1) == list(c.alloc(a, 1))
+            if rnd <= a:
+                assert o.alloc(a, 1) == list(c.alloc(a, 1))
     items = [(a, o.block_table(a)) for a in range(4)]
     assert c.offload_batch(items) == o.offload_batch(items)
     for rep in range(3):
