@@ -224,7 +224,9 @@ tc_status tc_reserve_info(tc_pool *p, tc_handle h, int64_t *reserved, int64_t *t
    decode while any of its blocks are host-resident or in flight").  tc_query: TC_OK if it has completed, TC_E_BUSY
    if not, TC_E_HANDLE if the handle is unknown (or forgotten, reading B3).  tc_wait: host-blocking wait.
    tc_stream_wait: makes `cuda_stream` wait GPU-side (no host block) — the engine's decode of an uploaded agent is
-   enqueued after it and reads the scattered blocks and remapped table.  No state changes. */
+   enqueued after it and reads the scattered blocks and remapped table.  No state changes.  In a staged batch that
+   runs as several pieces, each handle completes with the piece holding its last block, not with the whole batch,
+   and each piece waits only for the handles / agents it holds (TC_FINE_DEPS=0: batch granularity). */
 tc_status tc_query(tc_pool *p, tc_handle h);
 tc_status tc_wait(tc_pool *p, tc_handle h);                        /* host-blocking */
 tc_status tc_stream_wait(tc_pool *p, tc_handle h, void *cuda_stream); /* GPU-side dependency, no host block */
