@@ -270,6 +270,41 @@ def link_probe(torch, dev, dist, rank, world):
     return alone, conc
 
 
+def resume_probe(torch, dev, pool, cycle, ups, per_cycle, n=6):
+    """When can each agent of a cycle resume?  n drained cycles after the timed region: a side stream per upload
+    handle waits on it (tc_stream_wait, as an engine's decode of that agent would) and records an event; ms from the
+    cycle's start (an event on the upload stream just before tc_cycle) to the first / median / last agent, p50."""
+    sides = [torch.cuda.Stream(dev) for _ in range(max(1, per_cycle))]
+    rows = []
+    for _ in range(n):
+        pool.sync()
+        t0 = torch.cuda.Event(enable_timing=True)
+        evs = []
+
+        def rec(what):
+            if what == "start":
+                t0.record(ups)
+
+        def on_up(hs):
+            for h, st in zip(hs, sides):
+                pool.stream_wait(int(h), st.cuda_stream)
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(st)
+                evs.append(e)
+
+        cycle(record=rec, retire="sync", on_uploads=on_up)
+        torch.cuda.synchronize(dev)
+        if evs:
+            t = sorted(t0.elapsed_time(e) for e in evs)
+            rows.append((t[0], t[len(t) // 2], t[-1]))
+    if not rows:
+        return None
+    return {"first_ms": statistics.median(r[0] for r in rows), "median_ms": statistics.median(r[1] for r in rows),
+            "last_ms": statistics.median(r[2] for r in rows), "cycles": len(rows),
+            "how": "drained cycles after the timed region: per upload handle a side stream behind tc_stream_wait "
+                   "records an event; ms from the cycle's start to the first / median / last agent's resume, p50"}
+
+
 def offload_size_sweep(pool, cfg, B, sizes=None, reps=8):
     """C5's "sweep 1-512 blocks per offload" (BASELINE configs[4]; the Fig. 11 micro-benchmark): two
     sweep agents grown interleaved one block at a time (physically scattered ids); per size s and rep one tc_cycle
@@ -434,7 +469,7 @@ def run_ours(args):
     refused = {"nohost": 0, "noblocks": 0}     # why (first refusal of each laddered cycle)
     lag = [1]
 
-    def cycle(record=None, retire="sync"):
+    def cycle(record=None, retire="sync", on_uploads=None):
         """One scheduling cycle through the public API (tc_cycle: uploads then offloads), then its retirement point:
         retire = "sync" (tc_sync: drain and retire everything) or "retire" (tc_retire: retire what was enqueued
         before the previous point); returns (blocks_up, blocks_off)."""
@@ -473,6 +508,8 @@ def run_ours(args):
                 for a, h, t in zip(ags, out_h, tabs):
                     handles[int(a)] = int(h)
                     sizes[int(h)] = len(t)
+                if on_uploads is not None:
+                    on_uploads(hs)
                 nu += int(uoff[-1])
                 no += int(ooff[-1])
             elif op[0] == "sync":
@@ -616,6 +653,7 @@ def run_ours(args):
     # the link re-measured after the timed region (all ranks at once, best of 3): a box whose link drifts shows it
     # here, next to the pre-loop best-of-10 peak that is the denominator of roofline_link
     link_after = None if (args.quick or not link) else hostlink_peak(torch, dev, reps=3)
+    resume = None if args.quick else resume_probe(torch, dev, pool, cycle, ups, cfg.per_cycle)
     sweep = None
     if cfg.name == "c5" and not args.no_sweep:      # BASELINE configs[4]: 1-512 blocks per offload (every rank)
         if dist is not None:
@@ -781,6 +819,7 @@ def run_ours(args):
         "hostlink_peak": link,
         "hostlink_peak_alone": link_alone,
         "hostlink_peak_after": link_after,
+        "resume": resume,
         "sweep": sweep,
         "roofline": roof,
         "roofline_link": link_roof,
