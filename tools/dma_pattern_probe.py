@@ -30,7 +30,7 @@ def main():
     s_up, s_off, s_k = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     half = slab_gib // 2 * G
 
-    def run(piece_mib, kernels, secs=2.0):
+    def run(piece_mib, kernels, secs=2.0, pingpong=False):
         P = piece_mib << 20
         n = int(secs * 50e9 / P) + 1                            # pieces per direction for ~secs at 50 GB/s
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -41,8 +41,14 @@ def main():
             hb = (i * P) % (half - P)
             db = (i % 2) * (G // 2)
             seg = min(P, G // 2)
-            with torch.cuda.stream(s_up):                       # upload: slab -> staging half
-                stg_up[db:db + seg].copy_(host[hb:hb + seg], non_blocking=True)
+            if pingpong:                                        # upload what the offload wrote k pieces earlier
+                k = 8
+                src = half + ((i - k) * P) % (half - P) if i >= k else hb
+                with torch.cuda.stream(s_up):
+                    stg_up[db:db + seg].copy_(host[src:src + seg], non_blocking=True)
+            else:
+                with torch.cuda.stream(s_up):                   # upload: slab -> staging half
+                    stg_up[db:db + seg].copy_(host[hb:hb + seg], non_blocking=True)
             with torch.cuda.stream(s_off):                      # offload: staging half -> slab (other half)
                 host[half + hb:half + hb + seg].copy_(stg_off[db:db + seg], non_blocking=True)
             if kernels:                                         # HBM traffic of a gather + a scatter per piece
@@ -54,13 +60,15 @@ def main():
         torch.cuda.synchronize()
         up = n * min(P, G // 2) / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9
         off = n * min(P, G // 2) / (ev[2].elapsed_time(ev[3]) * 1e-3) / 1e9
-        return {"piece_mib": piece_mib, "kernels": kernels, "pieces": n, "h2d_gbs": round(up, 2),
+        return {"piece_mib": piece_mib, "kernels": kernels, "pingpong": pingpong, "pieces": n, "h2d_gbs": round(up, 2),
                 "d2h_gbs": round(off, 2), "both_gbs": round(up + off, 2)}
 
     run(512, False, 0.5)                                        # warm-up
     for piece in (512, 128, 32):
         for k in (False, True):
             print(json.dumps(run(piece, k)), flush=True)
+    for k in (False, True):                                     # uploads of recently offloaded host memory
+        print(json.dumps(run(512, k, pingpong=True)), flush=True)
     import os
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
