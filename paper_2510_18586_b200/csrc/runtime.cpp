@@ -258,9 +258,11 @@ tc_status Pool::create(const tc_pool_desc &d) {
     TC_CUDA(cudaSetDevice(device), "cudaSetDevice");
     int lo = 0, hi = 0;
     TC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
-    TC_CUDA(cudaStreamCreateWithPriority(&s_up, cudaStreamNonBlocking, hi), "upload stream");   // P:646 first
+    // TC_UP_PRIORITY=0: the upload streams at the default priority too (A/B of the copy-engine behaviour)
+    const int up_prio = env_int("TC_UP_PRIORITY", 1) ? hi : lo;
+    TC_CUDA(cudaStreamCreateWithPriority(&s_up, cudaStreamNonBlocking, up_prio), "upload stream");   // P:646 first
     TC_CUDA(cudaStreamCreateWithPriority(&s_off, cudaStreamNonBlocking, lo), "offload stream");
-    TC_CUDA(cudaStreamCreateWithPriority(&s_up_k, cudaStreamNonBlocking, hi), "upload aux stream");
+    TC_CUDA(cudaStreamCreateWithPriority(&s_up_k, cudaStreamNonBlocking, up_prio), "upload aux stream");
     TC_CUDA(cudaStreamCreateWithPriority(&s_off_k, cudaStreamNonBlocking, lo), "offload aux stream");
     piece_bytes = env_int("TC_PIECE_KIB", 256 * 1024) * 1024ll;
     head_bytes = env_int("TC_HEAD_KIB", 0) * 1024ll;

@@ -27,7 +27,10 @@ def main():
     stg_up = torch.empty(G, dtype=torch.uint8, device=dev)       # two 512 MiB halves per direction
     stg_off = torch.empty(G, dtype=torch.uint8, device=dev)
     pool = torch.empty(4 * G, dtype=torch.uint8, device=dev)
-    s_up, s_off, s_k = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    import os
+    hi = os.environ.get("PROBE_UP_PRIORITY") == "1"             # the library's upload streams run at high priority
+    s_up = torch.cuda.Stream(dev, priority=-1 if hi else 0)
+    s_off, s_k = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     half = slab_gib // 2 * G
 
     def run(piece_mib, kernels, secs=2.0, pingpong=False):
@@ -69,7 +72,6 @@ def main():
             print(json.dumps(run(piece, k)), flush=True)
     for k in (False, True):                                     # uploads of recently offloaded host memory
         print(json.dumps(run(512, k, pingpong=True)), flush=True)
-    import os
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import bench                                                # the bench's own link probe, same box, same call
