@@ -70,7 +70,7 @@ def parse():
                          "slots and blocks fit (judged from the warm-up cycles)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--quick", action="store_true", help="skip host-link probe and device-tier microbench")
+    ap.add_argument("--quick", action="store_true", help="skip the host-link probes (before and after), the device-tier microbench and the resume probe")
     ap.add_argument("--no-sweep", action="store_true", help="c5: skip the 1-512 blocks-per-offload sweep")
     ap.add_argument("--head-shards", type=int, default=0,
                     help="c4 on one GPU: run one rank's shard of a G-GPU head-sharded run (G = 1, 2, 4, 8) — the work "
